@@ -1,0 +1,88 @@
+"""Host-side formulas of the hot path, fp64/integer — TEST INFRASTRUCTURE ONLY.
+
+(See oracle/__init__.py for the usage rule.)
+
+  * causal pair count of a chunk   — S:43-50 [cost_model.forward_flops, c_lin = 0];
+    P:256 [§3.2] "the computational load for later token positions ... is heavier".
+  * FLOP convention                — BASELINE.md: fwd 4d per causal (q,k) pair,
+    bwd 10d per pair (2.5x fwd incl. the QK^T recompute).
+  * equal partition                — P:253 [§3.2] "length-based policy";
+    S:112-120 [partitioner.partition_equal], remainder to the first chunks.
+  * offload ratio alpha            — P:371-377 [§5.2] "alpha_i * A_i = M_threshold";
+    S:238-246 [offload_planner.compute_offload_ratios]; reading L9 for the last chunk.
+  * memory recurrence              — P:373 [§5.2] M_i = M_{i-1} + A_i - alpha_{i-1} A_{i-1};
+    S:247-254 [offload_planner.memory_timeline].
+"""
+
+from __future__ import annotations
+
+
+def causal_pairs(s_len: int, prefix: int) -> int:
+    """Causal (q,k) pairs of a chunk of s_len rows whose first row sits after
+    ``prefix`` earlier tokens: sum_{t=1}^{s_len} (prefix + t)."""
+    if s_len < 1 or prefix < 0:
+        raise ValueError("s_len >= 1 and prefix >= 0 required")
+    return sum(prefix + t for t in range(1, s_len + 1))
+
+
+def total_pairs(offsets) -> int:
+    """Sum over chunks of causal_pairs(s_i, c_i)."""
+    offsets = [int(x) for x in offsets]
+    return sum(causal_pairs(offsets[i + 1] - offsets[i], offsets[i]) for i in range(len(offsets) - 1))
+
+
+def attention_flops(heads: int, head_dim: int, offsets, part: str = "fwd+bwd") -> int:
+    """Algorithmic FLOPs: 4 d per pair (QK^T + PV) forward, 10 d per pair
+    backward (QK^T recompute, dV, dP, dQ, dK), per head."""
+    per_pair = {"fwd": 4, "bwd": 10, "fwd+bwd": 14}[part] * head_dim
+    return heads * per_pair * total_pairs(offsets)
+
+
+def partition_equal(S: int, N: int):
+    """Chunk lengths differing by at most 1, the first S mod N chunks one longer
+    (S:116-119).  Returns the list of lengths."""
+    if not (1 <= N <= S):
+        raise ValueError("1 <= N <= S required")
+    base, rem = divmod(S, N)
+    return [base + (1 if i < rem else 0) for i in range(N)]
+
+
+def offsets_from_lengths(lengths):
+    """c_0 = 0, c_{i+1} = c_i + s_i."""
+    out = [0]
+    for s in lengths:
+        if s < 1:
+            raise ValueError("chunk lengths must be >= 1")
+        out.append(out[-1] + int(s))
+    return out
+
+
+def offload_alpha(A, m_threshold: float, last: float = 1.0):
+    """alpha_i = min(1, M_threshold / A_i) for i < last chunk;
+    A_i = 0 gives alpha_i = 1 (nothing to offload).  The last chunk's
+    ratio is ``last``: 1.0 per the paper ("alpha_k = 1 for final
+    subsequence"), 0.0 in the single-layer bench (reading L9: its backward
+    consumes it immediately)."""
+    n = len(A)
+    out = []
+    for i, a in enumerate(A):
+        if i == n - 1:
+            out.append(float(last))
+        elif a <= 0:
+            out.append(1.0)
+        else:
+            out.append(min(1.0, float(m_threshold) / float(a)))
+    return out
+
+
+def memory_timeline(A, alpha):
+    """M_i = M_{i-1} + A_i - alpha_{i-1} A_{i-1}, M_{-1} = 0."""
+    if len(A) != len(alpha):
+        raise ValueError("length mismatch")
+    M = []
+    prev = 0.0
+    for i, a in enumerate(A):
+        shed = alpha[i - 1] * A[i - 1] if i > 0 else 0.0
+        prev = prev + a - shed
+        M.append(prev)
+    return M
