@@ -1,0 +1,91 @@
+// Internal launch interfaces between the C-ABI runtime (sppo_api.cu) and the
+// kernels.  Not part of the public ABI (include/sppo.h is).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sppo {
+
+// Maximum number of prior-KV chunks in one window (one launch).  A caller
+// with more chunks splits the prior set into several FIRST..LAST windows.
+constexpr int kMaxWindow = 256;
+
+// Window description carried in the kernel parameter block (by value).
+struct KvWindow {
+  int32_t n;                  // chunks in this window
+  int32_t start[kMaxWindow];  // absolute position c_j of the chunk's first key
+  int32_t len[kMaxWindow];    // s_j
+  const void* k[kMaxWindow];  // [s_j, heads, d]
+  const void* v[kMaxWindow];
+};
+
+struct KvGradWindow {
+  float* dk[kMaxWindow];  // fp32 accumulators [s_j, heads, d], +=
+  float* dv[kMaxWindow];
+};
+
+struct FwdParams {
+  int32_t heads, d;
+  int32_t q_start, q_len;  // c_i, s_i
+  float scale;             // tau
+  int32_t first, last;
+  const void* q;
+  void* o;
+  float* lse;
+  float* o_acc;  // carry (unnormalised), may be null when first&&last
+  float* m;
+  float* l;
+};
+
+struct BwdParams {
+  int32_t heads, d;
+  int32_t q_start, q_len;
+  float scale;
+  int32_t first, last;
+  const void* q;
+  const void* o;
+  const float* lse;
+  const void* dout;
+  float* delta;
+  float* dq_acc;
+  void* dq;
+  int32_t final_slot;  // window slot holding chunk i when dk/dv outputs are requested, else -1
+  void* dk_out;
+  void* dv_out;
+};
+
+// ---- SIMT kernels (fp32 path; exact FP32 FMA, no tensor cores) ----------
+cudaError_t launch_fwd_simt_f32(const FwdParams& p, const KvWindow& w, cudaStream_t s);
+cudaError_t launch_bwd_simt_f32(const BwdParams& p, const KvWindow& w, const KvGradWindow& g,
+                                cudaStream_t s);
+
+// ---- sm_100a tensor-core kernels (bf16, d = 128) -------------------------
+// Descriptor tables (CUtensorMap, 128 B each) live in device memory owned by
+// the ctx; kernels receive slot indices.
+struct TmaSlots {
+  uint16_t k[kMaxWindow];
+  uint16_t v[kMaxWindow];
+};
+
+struct Sm100Fwd {
+  FwdParams p;
+  const void* desc_table;  // device array of CUtensorMap
+  int32_t q_slot;          // descriptor slot of Q_i
+  int32_t n;               // window size
+  int32_t start[kMaxWindow];
+  int32_t len[kMaxWindow];
+  TmaSlots slots;
+};
+
+cudaError_t launch_fwd_sm100(const Sm100Fwd& a, cudaStream_t s);
+cudaError_t launch_bwd_sm100(const BwdParams& p, const KvWindow& w, const KvGradWindow& g,
+                             const void* desc_table, const TmaSlots& slots, int32_t q_slot,
+                             int32_t do_slot, cudaStream_t s);
+
+// ---- elementwise helpers (bwd pre/post-processing, memory-bound) ---------
+// delta[h, r] = sum_d dO[r,h,d] * O[r,h,d]; optionally zero dq_acc.
+cudaError_t launch_bwd_preprocess(const BwdParams& p, bool bf16, cudaStream_t s);
+// dst(dtype) = src(fp32), n elements (n % 4 == 0 fast path).
+cudaError_t launch_cast_f32(const float* src, void* dst, size_t n, bool bf16, cudaStream_t s);
+
+}  // namespace sppo

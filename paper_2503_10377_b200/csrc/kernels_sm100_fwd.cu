@@ -1,0 +1,331 @@
+// sm_100a tensor-core forward of chunked causal attention.
+//
+// Method: P:356 [§5.1] — chunk i's queries attend causally to K_j, V_j of the
+// chunks j <= i in the window; online softmax across KV tiles (FlashAttention,
+// P:134); O = softmax * V, LSE = m + ln l (readings L1, L2, L5).
+//
+// B200 design:
+//   CTA = 2 Q tiles x 128 rows of one head, 384 threads, 1 CTA / SM.
+//   warp 0      : TMA producer (Q once; K, V tiles through 2-stage rings)
+//   warp 1      : MMA issuer (one thread): S_t = Q_t K^T and O_t += P_t V,
+//                 tcgen05.mma kind::f16, M=128 N=128 K=16, fp32 accum in TMEM
+//   warp 2      : TMEM allocator (512 columns: S0, S1, O0, O1)
+//   warps 4-7   : softmax + epilogue of Q tile 0 (one TMEM lane = one row)
+//   warps 8-11  : softmax + epilogue of Q tile 1
+// P (bf16) overwrites the first 64 columns of its S tile and feeds the PV MMA
+// straight from TMEM (A operand); the two Q tiles ping-pong so the tensor core
+// computes one tile's MMAs while the other tile's softmax runs.  O is rescaled
+// lazily (only when a row max grows by > 8 in log2 units; exact because O and
+// l share the stale max).
+#include <cuda.h>
+#include <math.h>
+
+#include "internal.h"
+#include "sm100_ptx.cuh"
+
+namespace sppo {
+namespace {
+using namespace ptx;
+
+constexpr int BM = 128;                          // rows per Q tile
+constexpr int BN = 128;                          // keys per KV tile
+constexpr int HD = 128;                          // head dim
+constexpr int kThreads = 384;
+constexpr uint32_t kTileBytes = BM * HD * 2;     // 32 KB (two 16 KB SW128 boxes)
+constexpr uint32_t kHalf = kTileBytes / 2;       // one box: 128 rows x 64 cols
+constexpr int kSmemBytes = 6 * kTileBytes + 1024;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescaleThreshold = 8.0f;        // log2 units
+
+constexpr uint32_t kIdescS = idesc_bf16(128, 128, 0, 0);   // Q (K-major) x K (K-major)
+constexpr uint32_t kIdescPV = idesc_bf16(128, 128, 0, 1);  // P (TMEM) x V (MN-major)
+
+struct Bars {
+  uint64_t q_full;
+  uint64_t k_full[2], k_empty[2];
+  uint64_t v_full[2], v_empty[2];
+  uint64_t s_full[2];   // S_t ready in TMEM (per Q tile)
+  uint64_t p_full[2];   // P_t written to TMEM (128 softmax threads arrive)
+  uint64_t o_full[2];   // PV_t complete
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ const CUtensorMap* tmap(const Sm100Fwd& a, int slot) {
+  return reinterpret_cast<const CUtensorMap*>(a.desc_table) + slot;
+}
+
+// KV tile cursor over the window: chunks in order, 128-key tiles within each.
+struct TileCursor {
+  int c, tt;
+  __device__ TileCursor() : c(0), tt(0) {}
+  __device__ void next(const Sm100Fwd& a) {
+    if ((tt + 1) * BN < a.len[c]) {
+      ++tt;
+    } else {
+      ++c;
+      tt = 0;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant__ Sm100Fwd a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                       // Q0, Q1
+  uint8_t* sK = smem + 2 * kTileBytes;      // 2 stages
+  uint8_t* sV = smem + 4 * kTileBytes;      // 2 stages
+  __shared__ Bars bars;
+
+  const FwdParams& p = a.p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int head = blockIdx.y;
+  const int r0 = blockIdx.x * (2 * BM);  // first local row of Q tile 0
+
+  // ---- per-CTA tile counts (the diagonal chunk is last in the window)
+  int T[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int first_row = r0 + t * BM;
+    if (first_row >= p.q_len) {
+      T[t] = 0;
+      continue;
+    }
+    const int last_pos = p.q_start + min(first_row + BM, p.q_len) - 1;
+    int n = 0;
+    for (int c = 0; c < a.n; ++c) {
+      const int st = a.start[c], ln = a.len[c];
+      const int hi = min(st + ln - 1, last_pos);  // last visible key of this chunk
+      if (hi >= st) n += (hi - st) / BN + 1;
+    }
+    T[t] = n;
+  }
+  const int Tn = max(T[0], T[1]);
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars.q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars.k_full[s], 1);
+      mbar_init(&bars.k_empty[s], 1);
+      mbar_init(&bars.v_full[s], 1);
+      mbar_init(&bars.v_empty[s], 1);
+      mbar_init(&bars.s_full[s], 1);
+      mbar_init(&bars.p_full[s], 128);
+      mbar_init(&bars.o_full[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&bars.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars.tmem_base;
+  const uint32_t tS[2] = {tmem + 0, tmem + 128};
+  const uint32_t tO[2] = {tmem + 256, tmem + 384};
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      const CUtensorMap* mq = tmap(a, a.q_slot);
+      prefetch_tmap(mq);
+      mbar_arrive_expect_tx(&bars.q_full, 2 * kTileBytes);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        tma_load_3d(sQ + t * kTileBytes, mq, &bars.q_full, 0, head, r0 + t * BM);
+        tma_load_3d(sQ + t * kTileBytes + kHalf, mq, &bars.q_full, 64, head, r0 + t * BM);
+      }
+      TileCursor cur;
+      for (int n = 0; n < Tn; ++n, cur.next(a)) {
+        const int s = n & 1;
+        const uint32_t ph = (n >> 1) & 1;
+        const CUtensorMap* mk = tmap(a, a.slots.k[cur.c]);
+        const CUtensorMap* mv = tmap(a, a.slots.v[cur.c]);
+        const int row = cur.tt * BN;
+        mbar_wait(&bars.k_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&bars.k_full[s], kTileBytes);
+        tma_load_3d(sK + s * kTileBytes, mk, &bars.k_full[s], 0, head, row);
+        tma_load_3d(sK + s * kTileBytes + kHalf, mk, &bars.k_full[s], 64, head, row);
+        mbar_wait(&bars.v_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&bars.v_full[s], kTileBytes);
+        tma_load_3d(sV + s * kTileBytes, mv, &bars.v_full[s], 0, head, row);
+        tma_load_3d(sV + s * kTileBytes + kHalf, mv, &bars.v_full[s], 64, head, row);
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0 && Tn > 0) {
+      const uint32_t q_addr = smem_u32(sQ), k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+      auto issue_s = [&](int t, int stage) {
+        const uint32_t qa = q_addr + t * kTileBytes, ka = k_addr + stage * kTileBytes;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
+          mma_ss(tS[t], sdesc_kmajor(qa + off), sdesc_kmajor(ka + off), kIdescS, k > 0);
+        }
+        mma_commit(&bars.s_full[t]);
+      };
+      auto issue_pv = [&](int t, int stage, int n) {
+        const uint32_t va = v_addr + stage * kTileBytes;
+#pragma unroll
+        for (int k = 0; k < BN / 16; ++k)
+          mma_ts(tO[t], tS[t] + k * 8, sdesc_mnmajor(va + k * 2048, kHalf), kIdescPV, (n > 0 || k > 0) ? 1u : 0u);
+        mma_commit(&bars.o_full[t]);
+      };
+      mbar_wait(&bars.q_full, 0);
+      mbar_wait(&bars.k_full[0], 0);
+      tc_fence_after();
+      if (T[0] > 0) issue_s(0, 0);
+      if (T[1] > 0) issue_s(1, 0);
+      mma_commit(&bars.k_empty[0]);
+      for (int n = 0; n < Tn; ++n) {
+        const int vs = n & 1;
+        const int nx = n + 1, ks = nx & 1;
+        const uint32_t kph = (nx >> 1) & 1;
+        mbar_wait(&bars.v_full[vs], (n >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          if (n < T[t]) {
+            mbar_wait(&bars.p_full[t], n & 1);
+            tc_fence_after();
+            issue_pv(t, vs, n);
+            if (nx < T[t]) {
+              mbar_wait(&bars.k_full[ks], kph);
+              tc_fence_after();
+              issue_s(t, ks);
+            }
+          }
+        }
+        if (nx < Tn) mma_commit(&bars.k_empty[ks]);
+        mma_commit(&bars.v_empty[vs]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== softmax + epilogue =====================
+    const int t = (warp - 4) >> 2;                 // Q tile of this warpgroup
+    const int wq = warp & 3;                       // TMEM lane quarter
+    const int row_in_tile = wq * 32 + lane;
+    const int row = r0 + t * BM + row_in_tile;     // local row in chunk i
+    const int pos = p.q_start + row;               // absolute position
+    const float sl2 = p.scale * kLog2e;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const uint32_t sS = tS[t] + lane_off, sO = tO[t] + lane_off;
+    float m_used = -INFINITY, l = 0.f;
+    const int Tt = T[t];
+    TileCursor cur;
+    for (int n = 0; n < Tt; ++n, cur.next(a)) {
+      const int kpos0 = a.start[cur.c] + cur.tt * BN;
+      const int valid = min(BN, a.len[cur.c] - cur.tt * BN);
+      const int limit = min(valid, pos - kpos0 + 1);  // columns >= limit are masked
+      mbar_wait(&bars.s_full[t], n & 1);
+      tc_fence_after();
+      uint32_t r[128];
+      tmem_ld32(sS + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+      tmem_ld32(sS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+      tmem_ld32(sS + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
+      tmem_ld32(sS + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
+      tmem_wait_ld();
+      float* s = reinterpret_cast<float*>(r);
+      if (limit < BN) {
+#pragma unroll
+        for (int j = 0; j < BN; ++j) s[j] = (j < limit) ? s[j] : -INFINITY;
+      }
+      float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+#pragma unroll
+      for (int j = 4; j < BN; j += 4) {
+        mx0 = fmaxf(mx0, s[j]);
+        mx1 = fmaxf(mx1, s[j + 1]);
+        mx2 = fmaxf(mx2, s[j + 2]);
+        mx3 = fmaxf(mx3, s[j + 3]);
+      }
+      const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      if (n == 0) {
+        m_used = (mx == -INFINITY) ? 0.f : mx;
+      } else {
+        const bool need = mx > m_used + kRescaleThreshold;
+        if (__any_sync(0xffffffffu, need)) {
+          const float f = need ? ex2(m_used - mx) : 1.f;
+          if (need) {
+            m_used = mx;
+            l *= f;
+          }
+          mbar_wait(&bars.o_full[t], (n - 1) & 1);  // PV(n-1) finished writing O
+          tc_fence_after();
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) {
+            uint32_t o[32];
+            tmem_ld32(sO + cb * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * f);
+            tmem_st32(sO + cb * 32, o);
+          }
+          tmem_wait_st();
+        }
+      }
+      const float neg_m = -m_used;
+      float ls0 = 0.f, ls1 = 0.f;
+      uint32_t pk[64];
+#pragma unroll
+      for (int j = 0; j < BN; j += 2) {
+        const float e0 = ex2(fmaf(s[j], sl2, neg_m));
+        const float e1 = ex2(fmaf(s[j + 1], sl2, neg_m));
+        ls0 += e0;
+        ls1 += e1;
+        pk[j >> 1] = pack_bf16(e0, e1);
+      }
+      l += ls0 + ls1;
+      tmem_st32(sS + 0, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+      tmem_st32(sS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&bars.p_full[t]);
+    }
+    if (Tt > 0) {
+      mbar_wait(&bars.o_full[t], (Tt - 1) & 1);
+      tc_fence_after();
+      const bool ok = row < p.q_len;
+      const float inv = 1.f / l;
+      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + ((size_t)row * p.heads + head) * HD;
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) {
+        uint32_t o[32];
+        tmem_ld32(sO + cb * 32, o);
+        tmem_wait_ld();
+        if (ok) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + cb * 32);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint4 w;
+            w.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
+            w.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
+            w.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
+            w.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
+            dst[v] = w;
+          }
+        }
+      }
+      if (ok) p.lse[(size_t)head * p.q_len + row] = (m_used + __log2f(l)) * 0.6931471805599453f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace
+
+cudaError_t launch_fwd_sm100(const Sm100Fwd& a, cudaStream_t s) {
+  if (a.p.d != HD) return cudaErrorNotSupported;
+  if (!(a.p.first && a.p.last)) return cudaErrorNotSupported;  // split windows: TODO carry state
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  dim3 grid((a.p.q_len + 2 * BM - 1) / (2 * BM), a.p.heads);
+  fwd_kernel<<<grid, kThreads, kSmemBytes, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace sppo

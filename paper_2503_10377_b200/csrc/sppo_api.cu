@@ -1,0 +1,550 @@
+// C-ABI runtime of the SPPO hot path (include/sppo.h): argument validation,
+// FIRST/LAST window-coverage tracking, TMA descriptor cache, dispatch to the
+// kernels, pinned host arena and the D2H/H2D copy streams of the two-level
+// activation manager, host plan helpers.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/sppo.h"
+#include "internal.h"
+
+using namespace sppo;
+
+// ---------------------------------------------------------------- errors
+namespace {
+thread_local char g_err[512] = "";
+
+sppo_status fail(sppo_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+sppo_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(SPPO_E_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define SPPO_CUDA(call, what)                      \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+bool aligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
+
+// ---------------------------------------------------------------- TMA descriptors
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+struct DescKey {
+  const void* ptr;
+  int64_t rows;
+  int32_t heads, d, box_rows;
+  bool operator==(const DescKey& o) const {
+    return ptr == o.ptr && rows == o.rows && heads == o.heads && d == o.d && box_rows == o.box_rows;
+  }
+};
+struct DescKeyHash {
+  size_t operator()(const DescKey& k) const {
+    size_t h = std::hash<const void*>()(k.ptr);
+    h ^= std::hash<int64_t>()(k.rows * 1000003 + k.heads * 131 + k.d * 7 + k.box_rows) + 0x9e3779b97f4a7c15ull +
+         (h << 6) + (h >> 2);
+    return h;
+  }
+};
+
+constexpr int kDescSlots = 4096;
+
+struct Coverage {
+  int32_t chunk;
+  std::vector<uint8_t> seen;  // 0..chunk
+};
+
+}  // namespace
+
+struct sppo_ctx_s {
+  int device = 0;
+  cudaStream_t d2h = nullptr, h2d = nullptr;
+  cudaEvent_t ev_prod = nullptr, ev_cons = nullptr, ev_copy = nullptr;
+  // TMA descriptor cache: device table + pinned staging (one slot each).
+  CUtensorMap* desc_dev = nullptr;
+  CUtensorMap* desc_host = nullptr;
+  std::unordered_map<DescKey, int, DescKeyHash> desc_map;
+  std::vector<DescKey> desc_keys;
+  int desc_next = 0;
+  // window coverage per (direction, q pointer)
+  std::unordered_map<const void*, Coverage> cov_fwd, cov_bwd;
+  std::unordered_set<void*> host_allocs;
+  std::mutex mu;
+};
+
+namespace {
+
+// Returns the descriptor slot for a token-major [rows, heads, d] bf16 tensor,
+// tiled as boxes of {64 elements of d (128 B, SWIZZLE_128B), 1 head, box_rows}.
+// A new descriptor is staged in pinned memory and copied to the device table
+// on `stream` (stream-ordered before the kernel that uses it).
+sppo_status get_desc(sppo_ctx ctx, const void* ptr, int64_t rows, int heads, int d, int box_rows,
+                     cudaStream_t stream, int* slot) {
+  DescKey key{ptr, rows, heads, d, box_rows};
+  auto it = ctx->desc_map.find(key);
+  if (it != ctx->desc_map.end()) {
+    *slot = it->second;
+    return SPPO_OK;
+  }
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(SPPO_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  if (ctx->desc_next >= kDescSlots) {
+    // Table full: wait for all in-flight kernels, then recycle every slot.
+    SPPO_CUDA(cudaDeviceSynchronize(), "descriptor cache recycle");
+    ctx->desc_map.clear();
+    ctx->desc_next = 0;
+  }
+  const int s = ctx->desc_next++;
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)heads, (cuuint64_t)rows};
+  cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)heads * d * 2};
+  cuuint32_t box[3] = {64, 1, (cuuint32_t)box_rows};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&ctx->desc_host[s], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SPPO_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  SPPO_CUDA(cudaMemcpyAsync(&ctx->desc_dev[s], &ctx->desc_host[s], sizeof(CUtensorMap), cudaMemcpyHostToDevice,
+                            stream),
+            "descriptor upload");
+  ctx->desc_map[key] = s;
+  *slot = s;
+  return SPPO_OK;
+}
+
+// ---------------------------------------------------------------- validation
+sppo_status check_layout(const sppo_layout* L, int32_t chunk) {
+  if (!L) return fail(SPPO_E_ARG, "layout is NULL");
+  if (!L->offsets) return fail(SPPO_E_ARG, "layout.offsets is NULL");
+  if (L->heads < 1) return fail(SPPO_E_SHAPE, "layout.heads = %d < 1", L->heads);
+  if (L->dtype != SPPO_BF16 && L->dtype != SPPO_FP32) return fail(SPPO_E_ARG, "layout.dtype = %d", L->dtype);
+  if (L->dtype == SPPO_FP32 && L->head_dim != 32 && L->head_dim != 64 && L->head_dim != 128)
+    return fail(SPPO_E_UNSUPPORTED, "fp32 path supports head_dim 32/64/128, got %d", L->head_dim);
+  if (L->dtype == SPPO_BF16 && L->head_dim != 128)
+    return fail(SPPO_E_UNSUPPORTED, "bf16 tensor-core path supports head_dim 128, got %d", L->head_dim);
+  if (L->num_chunks < 1) return fail(SPPO_E_SHAPE, "layout.num_chunks = %d < 1", L->num_chunks);
+  if (L->offsets[0] != 0) return fail(SPPO_E_SHAPE, "offsets[0] = %lld != 0", (long long)L->offsets[0]);
+  for (int i = 0; i < L->num_chunks; ++i)
+    if (L->offsets[i + 1] <= L->offsets[i])
+      return fail(SPPO_E_SHAPE, "offsets not strictly increasing at %d", i);
+  if (L->offsets[L->num_chunks] > (int64_t)INT32_MAX) return fail(SPPO_E_SHAPE, "S exceeds 2^31-1");
+  if (!(L->scale >= 0.f) || !isfinite(L->scale)) return fail(SPPO_E_ARG, "scale must be finite and >= 0");
+  if (chunk < 0 || chunk >= L->num_chunks)
+    return fail(SPPO_E_SHAPE, "chunk %d outside [0, %d)", chunk, L->num_chunks);
+  return SPPO_OK;
+}
+
+sppo_status check_kv(const sppo_layout* L, int32_t chunk, const sppo_kv_set* kv, const Coverage* cov,
+                     bool first, bool last) {
+  if (!kv) return fail(SPPO_E_ARG, "kv set is NULL");
+  if (kv->n < 1) return fail(SPPO_E_ARG, "kv.n = %d < 1", kv->n);
+  if (kv->n > kMaxWindow) return fail(SPPO_E_UNSUPPORTED, "kv.n = %d > %d: split the window", kv->n, kMaxWindow);
+  if (!kv->ids || !kv->k || !kv->v) return fail(SPPO_E_ARG, "kv arrays are NULL");
+  std::vector<uint8_t> seen(chunk + 1, 0);
+  if (!first && cov) seen = cov->seen;
+  for (int c = 0; c < kv->n; ++c) {
+    const int j = kv->ids[c];
+    if (j < 0 || j > chunk) return fail(SPPO_E_SHAPE, "kv id %d not in [0, %d]", j, chunk);
+    if (!kv->k[c] || !kv->v[c]) return fail(SPPO_E_ARG, "kv buffer %d is NULL", c);
+    if (!aligned16(kv->k[c]) || !aligned16(kv->v[c])) return fail(SPPO_E_ALIGN, "kv buffer %d not 16B aligned", c);
+    if (seen[j]) return fail(SPPO_E_STATE, "chunk %d appears twice in the windows of chunk %d", j, chunk);
+    seen[j] = 1;
+  }
+  if (last)
+    for (int j = 0; j <= chunk; ++j)
+      if (!seen[j]) return fail(SPPO_E_STATE, "LAST window of chunk %d leaves chunk %d uncovered", chunk, j);
+  (void)L;
+  return SPPO_OK;
+}
+
+// Applies the window to the coverage map (called only after a successful enqueue).
+void commit_coverage(std::unordered_map<const void*, Coverage>& m, const void* key, int32_t chunk,
+                     const sppo_kv_set* kv, bool first, bool last) {
+  if (last) {
+    m.erase(key);
+    return;
+  }
+  Coverage& c = m[key];
+  if (first) {
+    c.chunk = chunk;
+    c.seen.assign(chunk + 1, 0);
+  }
+  for (int i = 0; i < kv->n; ++i) c.seen[kv->ids[i]] = 1;
+}
+
+sppo_status lookup_coverage(std::unordered_map<const void*, Coverage>& m, const void* key, int32_t chunk,
+                            bool first, const Coverage** out) {
+  *out = nullptr;
+  auto it = m.find(key);
+  if (first) {
+    if (it != m.end()) m.erase(it);  // a new FIRST abandons an unfinished chunk state
+    return SPPO_OK;
+  }
+  if (it == m.end() || it->second.chunk != chunk)
+    return fail(SPPO_E_STATE, "window of chunk %d without FIRST (no open state for this q)", chunk);
+  *out = &it->second;
+  return SPPO_OK;
+}
+
+void fill_window(const sppo_layout* L, const sppo_kv_set* kv, KvWindow* w) {
+  w->n = kv->n;
+  for (int c = 0; c < kv->n; ++c) {
+    const int j = kv->ids[c];
+    w->start[c] = (int32_t)L->offsets[j];
+    w->len[c] = (int32_t)(L->offsets[j + 1] - L->offsets[j]);
+    w->k[c] = kv->k[c];
+    w->v[c] = kv->v[c];
+  }
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+int32_t sppo_version(void) { return 100; }
+
+const char* sppo_last_error(void) { return g_err; }
+
+sppo_status sppo_ctx_create(int device, sppo_ctx* out) {
+  if (!out) return fail(SPPO_E_ARG, "out is NULL");
+  *out = nullptr;
+  int n = 0;
+  SPPO_CUDA(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+  if (device < 0 || device >= n) return fail(SPPO_E_ARG, "device %d not in [0, %d)", device, n);
+  SPPO_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  sppo_ctx c = new sppo_ctx_s();
+  c->device = device;
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&c->ev_prod, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&c->ev_cons, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaMalloc(&c->desc_dev, sizeof(CUtensorMap) * kDescSlots)) != cudaSuccess ||
+      (e = cudaHostAlloc(&c->desc_host, sizeof(CUtensorMap) * kDescSlots, cudaHostAllocDefault)) != cudaSuccess) {
+    sppo_ctx_destroy(c);
+    return cuda_fail(e, "sppo_ctx_create");
+  }
+  *out = c;
+  return SPPO_OK;
+}
+
+sppo_status sppo_ctx_destroy(sppo_ctx c) {
+  if (!c) return fail(SPPO_E_ARG, "ctx is NULL");
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (void* h : c->host_allocs) cudaFreeHost(h);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->ev_prod) cudaEventDestroy(c->ev_prod);
+  if (c->ev_cons) cudaEventDestroy(c->ev_cons);
+  if (c->ev_copy) cudaEventDestroy(c->ev_copy);
+  if (c->desc_dev) cudaFree(c->desc_dev);
+  if (c->desc_host) cudaFreeHost(c->desc_host);
+  delete c;
+  return SPPO_OK;
+}
+
+sppo_status sppo_ctx_sync(sppo_ctx c) {
+  if (!c) return fail(SPPO_E_ARG, "ctx is NULL");
+  SPPO_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  SPPO_CUDA(cudaDeviceSynchronize(), "device fault");
+  SPPO_CUDA(cudaGetLastError(), "device fault");
+  return SPPO_OK;
+}
+
+// ---------------------------------------------------------------- forward
+sppo_status sppo_attn_fwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, const void* q, const sppo_kv_set* kv,
+                          int32_t flags, const sppo_fwd_state* st, void* o, float* lse, void* stream) {
+  if (!ctx) return fail(SPPO_E_ARG, "ctx is NULL");
+  sppo_status s = check_layout(L, chunk);
+  if (s) return s;
+  if (flags & ~(SPPO_FIRST | SPPO_LAST)) return fail(SPPO_E_ARG, "unknown flags 0x%x", flags);
+  const bool first = flags & SPPO_FIRST, last = flags & SPPO_LAST;
+  if (!q) return fail(SPPO_E_ARG, "q is NULL");
+  if (!aligned16(q)) return fail(SPPO_E_ALIGN, "q not 16B aligned");
+  if (last && (!o || !lse)) return fail(SPPO_E_ARG, "o/lse NULL on LAST");
+  if (last && (!aligned16(o) || !aligned4(lse))) return fail(SPPO_E_ALIGN, "o not 16B / lse not 4B aligned");
+  const bool need_state = !(first && last);
+  if (need_state && (!st || !st->o_acc || !st->m || !st->l))
+    return fail(SPPO_E_ARG, "split windows need a carry state (o_acc, m, l)");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  const Coverage* cov = nullptr;
+  if ((s = lookup_coverage(ctx->cov_fwd, q, chunk, first, &cov))) return s;
+  if ((s = check_kv(L, chunk, kv, cov, first, last))) return s;
+  SPPO_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+
+  cudaStream_t strm = (cudaStream_t)stream;
+  FwdParams p{};
+  p.heads = L->heads;
+  p.d = L->head_dim;
+  p.q_start = (int32_t)L->offsets[chunk];
+  p.q_len = (int32_t)(L->offsets[chunk + 1] - L->offsets[chunk]);
+  p.scale = L->scale > 0.f ? L->scale : 1.f / sqrtf((float)L->head_dim);
+  p.first = first;
+  p.last = last;
+  p.q = q;
+  p.o = o;
+  p.lse = lse;
+  if (st) {
+    p.o_acc = st->o_acc;
+    p.m = st->m;
+    p.l = st->l;
+  }
+  cudaError_t e;
+  if (L->dtype == SPPO_FP32) {
+    static KvWindow w;  // large; guarded by ctx->mu
+    fill_window(L, kv, &w);
+    e = launch_fwd_simt_f32(p, w, strm);
+  } else {
+    if (!(first && last))
+      return fail(SPPO_E_UNSUPPORTED, "bf16 forward with split windows is not implemented yet (pass FIRST|LAST)");
+    static Sm100Fwd a;
+    a.p = p;
+    a.n = kv->n;
+    a.desc_table = ctx->desc_dev;
+    if ((s = get_desc(ctx, q, p.q_len, p.heads, p.d, 128, strm, &a.q_slot))) return s;
+    // kernel contract: the diagonal chunk (id == chunk), if present, is visited last
+    std::vector<int> order;
+    for (int c = 0; c < kv->n; ++c)
+      if (kv->ids[c] != chunk) order.push_back(c);
+    for (int c = 0; c < kv->n; ++c)
+      if (kv->ids[c] == chunk) order.push_back(c);
+    for (int oc = 0; oc < kv->n; ++oc) {
+      const int c = order[oc];
+      const int j = kv->ids[c];
+      const int64_t len = L->offsets[j + 1] - L->offsets[j];
+      a.start[oc] = (int32_t)L->offsets[j];
+      a.len[oc] = (int32_t)len;
+      int sk, sv;
+      if ((s = get_desc(ctx, kv->k[c], len, p.heads, p.d, 128, strm, &sk))) return s;
+      if ((s = get_desc(ctx, kv->v[c], len, p.heads, p.d, 128, strm, &sv))) return s;
+      a.slots.k[oc] = (uint16_t)sk;
+      a.slots.v[oc] = (uint16_t)sv;
+    }
+    e = launch_fwd_sm100(a, strm);
+  }
+  if (e == cudaErrorNotSupported) return fail(SPPO_E_UNSUPPORTED, "this request is not implemented by the sm_100a kernels");
+  if (e != cudaSuccess) return cuda_fail(e, "sppo_attn_fwd launch");
+  commit_coverage(ctx->cov_fwd, q, chunk, kv, first, last);
+  return SPPO_OK;
+}
+
+// ---------------------------------------------------------------- backward
+sppo_status sppo_attn_bwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, const void* q, const sppo_kv_set* kv,
+                          const sppo_bwd_args* a, int32_t flags, void* stream) {
+  if (!ctx) return fail(SPPO_E_ARG, "ctx is NULL");
+  sppo_status s = check_layout(L, chunk);
+  if (s) return s;
+  if (flags & ~(SPPO_FIRST | SPPO_LAST)) return fail(SPPO_E_ARG, "unknown flags 0x%x", flags);
+  const bool first = flags & SPPO_FIRST, last = flags & SPPO_LAST;
+  if (!q || !a) return fail(SPPO_E_ARG, "q/args is NULL");
+  if (!a->o || !a->lse || !a->dout || !a->delta || !a->dq_acc || !a->dk_acc || !a->dv_acc)
+    return fail(SPPO_E_ARG, "bwd args: o/lse/dout/delta/dq_acc/dk_acc/dv_acc must be non-NULL");
+  if (last && !a->dq) return fail(SPPO_E_ARG, "dq NULL on LAST");
+  if ((a->dk == nullptr) != (a->dv == nullptr)) return fail(SPPO_E_ARG, "dk and dv outputs must both be set or both NULL");
+  if (!aligned4(a->lse) || !aligned4(a->delta)) return fail(SPPO_E_ALIGN, "lse/delta not 4B aligned");
+  const void* ptrs[] = {q, a->o, a->dout, a->dq_acc, a->dq, a->dk, a->dv};
+  for (const void* pp : ptrs)
+    if (pp && !aligned16(pp)) return fail(SPPO_E_ALIGN, "bwd tensor not 16B aligned");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  const Coverage* cov = nullptr;
+  if ((s = lookup_coverage(ctx->cov_bwd, q, chunk, first, &cov))) return s;
+  if ((s = check_kv(L, chunk, kv, cov, first, last))) return s;
+  int final_slot = -1;
+  for (int c = 0; c < kv->n; ++c) {
+    if (!a->dk_acc[c] || !a->dv_acc[c]) return fail(SPPO_E_ARG, "dk_acc/dv_acc %d is NULL", c);
+    if (!aligned16(a->dk_acc[c]) || !aligned16(a->dv_acc[c])) return fail(SPPO_E_ALIGN, "dk_acc/dv_acc %d misaligned", c);
+    if (kv->ids[c] == chunk) final_slot = c;
+  }
+  if (a->dk && final_slot < 0)
+    return fail(SPPO_E_STATE, "dk/dv outputs requested but chunk %d is not in this window", chunk);
+  SPPO_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t strm = (cudaStream_t)stream;
+  BwdParams p{};
+  p.heads = L->heads;
+  p.d = L->head_dim;
+  p.q_start = (int32_t)L->offsets[chunk];
+  p.q_len = (int32_t)(L->offsets[chunk + 1] - L->offsets[chunk]);
+  p.scale = L->scale > 0.f ? L->scale : 1.f / sqrtf((float)L->head_dim);
+  p.first = first;
+  p.last = last;
+  p.q = q;
+  p.o = a->o;
+  p.lse = a->lse;
+  p.dout = a->dout;
+  p.delta = a->delta;
+  p.dq_acc = a->dq_acc;
+  p.dq = a->dq;
+  p.final_slot = a->dk ? final_slot : -1;
+  p.dk_out = a->dk;
+  p.dv_out = a->dv;
+  const bool bf16 = L->dtype == SPPO_BF16;
+  cudaError_t e = cudaSuccess;
+  if (first) e = launch_bwd_preprocess(p, bf16, strm);  // Delta_i, dq_acc = 0  (a5)
+  if (e != cudaSuccess) return cuda_fail(e, "bwd preprocess");
+  static KvWindow w;
+  static KvGradWindow g;
+  fill_window(L, kv, &w);
+  for (int c = 0; c < kv->n; ++c) {
+    g.dk[c] = a->dk_acc[c];
+    g.dv[c] = a->dv_acc[c];
+  }
+  if (!bf16) {
+    e = launch_bwd_simt_f32(p, w, g, strm);
+  } else {
+    static TmaSlots slots;
+    int q_slot, do_slot;
+    if ((s = get_desc(ctx, q, p.q_len, p.heads, p.d, 128, strm, &q_slot))) return s;
+    if ((s = get_desc(ctx, a->dout, p.q_len, p.heads, p.d, 128, strm, &do_slot))) return s;
+    for (int c = 0; c < kv->n; ++c) {
+      int sk, sv;
+      if ((s = get_desc(ctx, kv->k[c], w.len[c], p.heads, p.d, 128, strm, &sk))) return s;
+      if ((s = get_desc(ctx, kv->v[c], w.len[c], p.heads, p.d, 128, strm, &sv))) return s;
+      slots.k[c] = (uint16_t)sk;
+      slots.v[c] = (uint16_t)sv;
+    }
+    e = launch_bwd_sm100(p, w, g, ctx->desc_dev, slots, q_slot, do_slot, strm);
+  }
+  if (e == cudaErrorNotSupported) return fail(SPPO_E_UNSUPPORTED, "this request is not implemented by the sm_100a kernels");
+  if (e != cudaSuccess) return cuda_fail(e, "sppo_attn_bwd launch");
+  if (last) {
+    e = launch_cast_f32(p.dq_acc, p.dq, (size_t)p.q_len * p.heads * p.d, bf16, strm);  // a7
+    if (e != cudaSuccess) return cuda_fail(e, "dq finalize");
+  }
+  commit_coverage(ctx->cov_bwd, q, chunk, kv, first, last);
+  return SPPO_OK;
+}
+
+// ---------------------------------------------------------------- host arena + copies
+sppo_status sppo_host_alloc(sppo_ctx ctx, size_t bytes, void** host) {
+  if (!ctx || !host) return fail(SPPO_E_ARG, "ctx/host is NULL");
+  *host = nullptr;
+  if (!bytes) return fail(SPPO_E_ARG, "bytes = 0");
+  SPPO_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  void* p = nullptr;
+  cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+  if (e != cudaSuccess) return fail(SPPO_E_OOM, "cudaHostAlloc(%zu): %s", bytes, cudaGetErrorString(e));
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  ctx->host_allocs.insert(p);
+  *host = p;
+  return SPPO_OK;
+}
+
+sppo_status sppo_host_free(sppo_ctx ctx, void* host) {
+  if (!ctx || !host) return fail(SPPO_E_ARG, "ctx/host is NULL");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  auto it = ctx->host_allocs.find(host);
+  if (it == ctx->host_allocs.end()) return fail(SPPO_E_ARG, "pointer not from sppo_host_alloc");
+  ctx->host_allocs.erase(it);
+  SPPO_CUDA(cudaFreeHost(host), "cudaFreeHost");
+  return SPPO_OK;
+}
+
+sppo_status sppo_kv_offload(sppo_ctx ctx, int32_t chunk, const void* dev, void* host, size_t bytes, double alpha,
+                            void* producer, void* done, size_t* copied) {
+  if (!ctx || !dev || !host) return fail(SPPO_E_ARG, "ctx/dev/host is NULL");
+  if (chunk < 0) return fail(SPPO_E_ARG, "chunk < 0");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(SPPO_E_ARG, "alpha %g not in [0,1]", alpha);
+  const size_t granule = 64 << 10;
+  size_t n = (size_t)ceil(alpha * (double)bytes);
+  n = (n + granule - 1) / granule * granule;
+  if (n > bytes) n = bytes;
+  if (copied) *copied = n;
+  SPPO_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  SPPO_CUDA(cudaEventRecord(ctx->ev_prod, (cudaStream_t)producer), "offload: record producer");
+  SPPO_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->ev_prod, 0), "offload: wait producer");
+  if (n) SPPO_CUDA(cudaMemcpyAsync(host, dev, n, cudaMemcpyDeviceToHost, ctx->d2h), "offload: D2H copy");
+  if (done) SPPO_CUDA(cudaEventRecord((cudaEvent_t)done, ctx->d2h), "offload: record done");
+  return SPPO_OK;
+}
+
+sppo_status sppo_kv_prefetch(sppo_ctx ctx, int32_t chunk, const void* host, void* dev, size_t bytes, void* consumer,
+                             void* done) {
+  if (!ctx || !dev || !host) return fail(SPPO_E_ARG, "ctx/dev/host is NULL");
+  if (chunk < 0) return fail(SPPO_E_ARG, "chunk < 0");
+  SPPO_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaStream_t cons = (cudaStream_t)consumer;
+  SPPO_CUDA(cudaEventRecord(ctx->ev_cons, cons), "prefetch: record consumer");
+  SPPO_CUDA(cudaStreamWaitEvent(ctx->h2d, ctx->ev_cons, 0), "prefetch: wait consumer");
+  if (bytes) SPPO_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->h2d), "prefetch: H2D copy");
+  SPPO_CUDA(cudaEventRecord(ctx->ev_copy, ctx->h2d), "prefetch: record copy");
+  SPPO_CUDA(cudaStreamWaitEvent(cons, ctx->ev_copy, 0), "prefetch: consumer wait");
+  if (done) SPPO_CUDA(cudaEventRecord((cudaEvent_t)done, ctx->h2d), "prefetch: record done");
+  return SPPO_OK;
+}
+
+// ---------------------------------------------------------------- plan helpers
+sppo_status sppo_partition_equal(int64_t S, int32_t N, int64_t* out) {
+  if (!out) return fail(SPPO_E_ARG, "out is NULL");
+  if (N < 1 || S < N) return fail(SPPO_E_SHAPE, "need 1 <= N <= S (S=%lld, N=%d)", (long long)S, N);
+  const int64_t base = S / N, rem = S % N;
+  out[0] = 0;
+  for (int32_t i = 0; i < N; ++i) out[i + 1] = out[i] + base + (i < rem ? 1 : 0);
+  return SPPO_OK;
+}
+
+sppo_status sppo_causal_pairs(const int64_t* off, int32_t N, int64_t* pairs) {
+  if (!off || !pairs) return fail(SPPO_E_ARG, "NULL argument");
+  if (N < 1) return fail(SPPO_E_SHAPE, "N < 1");
+  int64_t total = 0;
+  for (int32_t i = 0; i < N; ++i) {
+    const int64_t c = off[i], s = off[i + 1] - off[i];
+    if (s < 1 || c < 0) return fail(SPPO_E_SHAPE, "offsets not strictly increasing at %d", i);
+    total += s * c + s * (s + 1) / 2;
+  }
+  *pairs = total;
+  return SPPO_OK;
+}
+
+sppo_status sppo_offload_alpha(const double* A, int32_t N, double m_threshold, double last, double* alpha) {
+  if (!A || !alpha) return fail(SPPO_E_ARG, "NULL argument");
+  if (N < 1) return fail(SPPO_E_SHAPE, "N < 1");
+  if (!(m_threshold >= 0.0)) return fail(SPPO_E_ARG, "m_threshold < 0");
+  if (!(last >= 0.0 && last <= 1.0)) return fail(SPPO_E_ARG, "last alpha not in [0,1]");
+  for (int32_t i = 0; i < N; ++i) {
+    if (i == N - 1)
+      alpha[i] = last;
+    else if (A[i] <= 0.0)
+      alpha[i] = 1.0;
+    else
+      alpha[i] = fmin(1.0, m_threshold / A[i]);
+  }
+  return SPPO_OK;
+}
+
+}  // extern "C"

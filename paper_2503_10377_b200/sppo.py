@@ -1,0 +1,230 @@
+"""ctypes binding of libsppo.so (include/sppo.h) — argument marshalling only.
+
+Every compute step runs in the CUDA kernels behind the C ABI; this module turns
+torch tensors into device pointers, Python lists into C arrays and non-OK
+statuses into exceptions.  It never computes anything itself and there is no
+fallback: if the native library is missing, importing it raises.
+
+Names follow the C ABI: sppo_attn_fwd -> Context.attn_fwd, etc.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsppo.so")
+
+SPPO_BF16, SPPO_FP32 = 0, 1
+SPPO_FIRST, SPPO_LAST = 1, 2
+
+STATUS = {0: "SPPO_OK", 1: "SPPO_E_ARG", 2: "SPPO_E_SHAPE", 3: "SPPO_E_ALIGN", 4: "SPPO_E_STATE",
+          5: "SPPO_E_NOT_RESIDENT", 6: "SPPO_E_OOM", 7: "SPPO_E_CUDA", 8: "SPPO_E_UNSUPPORTED"}
+
+# every symbol include/sppo.h declares
+EXPORTS = ("sppo_ctx_create", "sppo_ctx_destroy", "sppo_ctx_sync", "sppo_last_error", "sppo_version",
+           "sppo_attn_fwd", "sppo_attn_bwd", "sppo_host_alloc", "sppo_host_free", "sppo_kv_offload",
+           "sppo_kv_prefetch", "sppo_partition_equal", "sppo_causal_pairs", "sppo_offload_alpha")
+
+
+class SppoError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class _Layout(C.Structure):
+    _fields_ = [("heads", C.c_int32), ("head_dim", C.c_int32), ("dtype", C.c_int32), ("num_chunks", C.c_int32),
+                ("offsets", C.POINTER(C.c_int64)), ("scale", C.c_float)]
+
+
+class _KvSet(C.Structure):
+    _fields_ = [("n", C.c_int32), ("ids", C.POINTER(C.c_int32)), ("k", C.POINTER(C.c_void_p)),
+                ("v", C.POINTER(C.c_void_p))]
+
+
+class _FwdState(C.Structure):
+    _fields_ = [("o_acc", C.c_void_p), ("m", C.c_void_p), ("l", C.c_void_p)]
+
+
+class _BwdArgs(C.Structure):
+    _fields_ = [("o", C.c_void_p), ("lse", C.c_void_p), ("dout", C.c_void_p), ("delta", C.c_void_p),
+                ("dq_acc", C.c_void_p), ("dk_acc", C.POINTER(C.c_void_p)), ("dv_acc", C.POINTER(C.c_void_p)),
+                ("dq", C.c_void_p), ("dk", C.c_void_p), ("dv", C.c_void_p)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() (no CPU fallback exists)")
+    lib = C.CDLL(LIB_PATH)
+    i32, vp, sz = C.c_int32, C.c_void_p, C.c_size_t
+    sig = {
+        "sppo_ctx_create": ([C.c_int, C.POINTER(vp)], i32),
+        "sppo_ctx_destroy": ([vp], i32),
+        "sppo_ctx_sync": ([vp], i32),
+        "sppo_last_error": ([], C.c_char_p),
+        "sppo_version": ([], i32),
+        "sppo_attn_fwd": ([vp, C.POINTER(_Layout), i32, vp, C.POINTER(_KvSet), i32, C.POINTER(_FwdState), vp, vp, vp],
+                          i32),
+        "sppo_attn_bwd": ([vp, C.POINTER(_Layout), i32, vp, C.POINTER(_KvSet), C.POINTER(_BwdArgs), i32, vp], i32),
+        "sppo_host_alloc": ([vp, sz, C.POINTER(vp)], i32),
+        "sppo_host_free": ([vp, vp], i32),
+        "sppo_kv_offload": ([vp, i32, vp, vp, sz, C.c_double, vp, vp, C.POINTER(sz)], i32),
+        "sppo_kv_prefetch": ([vp, i32, vp, vp, sz, vp, vp], i32),
+        "sppo_partition_equal": ([C.c_int64, i32, C.POINTER(C.c_int64)], i32),
+        "sppo_causal_pairs": ([C.POINTER(C.c_int64), i32, C.POINTER(C.c_int64)], i32),
+        "sppo_offload_alpha": ([C.POINTER(C.c_double), i32, C.c_double, C.c_double, C.POINTER(C.c_double)], i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes, fn.restype = args, res
+    return lib
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise SppoError(st, _lib.sppo_last_error().decode(errors="replace"))
+
+
+def _ptr(t):
+    """Device/host pointer of a tensor (or int / None) — marshalling only."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    if not t.is_contiguous():
+        raise ValueError("tensors passed to the C ABI must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(s):
+    if s is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+def _event(e):
+    if e is None:
+        return None
+    if isinstance(e, int):
+        return e
+    return e.cuda_event
+
+
+# ------------------------------------------------------------------ plan helpers
+def partition_equal(S: int, N: int):
+    out = (C.c_int64 * (N + 1))()
+    _check(_lib.sppo_partition_equal(S, N, out))
+    return list(out)
+
+
+def causal_pairs(offsets) -> int:
+    arr = (C.c_int64 * len(offsets))(*offsets)
+    out = C.c_int64()
+    _check(_lib.sppo_causal_pairs(arr, len(offsets) - 1, C.byref(out)))
+    return out.value
+
+
+def offload_alpha(A, m_threshold: float, last: float = 1.0):
+    n = len(A)
+    a = (C.c_double * n)(*A)
+    out = (C.c_double * n)()
+    _check(_lib.sppo_offload_alpha(a, n, m_threshold, last, out))
+    return list(out)
+
+
+class Layout:
+    """sppo_layout: heads on this device, head_dim, dtype, chunk offsets."""
+
+    def __init__(self, heads: int, head_dim: int, offsets, dtype: int = SPPO_BF16, scale: float = 0.0):
+        self.offsets = [int(x) for x in offsets]
+        self._off = (C.c_int64 * len(self.offsets))(*self.offsets)
+        self.c = _Layout(heads, head_dim, dtype, len(self.offsets) - 1, self._off, scale)
+        self.heads, self.head_dim, self.dtype = heads, head_dim, dtype
+        self.num_chunks = len(self.offsets) - 1
+        self.scale = scale if scale else 1.0 / math.sqrt(head_dim)
+
+    def chunk_len(self, i: int) -> int:
+        return self.offsets[i + 1] - self.offsets[i]
+
+
+def _kvset(ids, ks, vs):
+    n = len(ids)
+    kv = _KvSet(n, (C.c_int32 * n)(*ids), (C.c_void_p * n)(*[_ptr(k) for k in ks]),
+                (C.c_void_p * n)(*[_ptr(v) for v in vs]))
+    return kv
+
+
+class Context:
+    """sppo_ctx: one per (device, host thread)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _check(_lib.sppo_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            _check(_lib.sppo_ctx_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sync(self):
+        _check(_lib.sppo_ctx_sync(self.h))
+
+    # -------------------------------------------------------------- attention
+    def attn_fwd(self, layout: Layout, chunk: int, q, kv_ids, ks, vs, flags=SPPO_FIRST | SPPO_LAST, state=None,
+                 o=None, lse=None, stream=None):
+        kv = _kvset(kv_ids, ks, vs)
+        st = None
+        if state is not None:
+            st = _FwdState(_ptr(state[0]), _ptr(state[1]), _ptr(state[2]))
+        _check(_lib.sppo_attn_fwd(self.h, C.byref(layout.c), chunk, _ptr(q), C.byref(kv), flags,
+                                  C.byref(st) if st is not None else None, _ptr(o), _ptr(lse), _stream(stream)))
+
+    def attn_bwd(self, layout: Layout, chunk: int, q, kv_ids, ks, vs, o, lse, dout, delta, dq_acc, dk_accs,
+                 dv_accs, dq=None, dk=None, dv=None, flags=SPPO_FIRST | SPPO_LAST, stream=None):
+        kv = _kvset(kv_ids, ks, vs)
+        n = len(kv_ids)
+        args = _BwdArgs(_ptr(o), _ptr(lse), _ptr(dout), _ptr(delta), _ptr(dq_acc),
+                        (C.c_void_p * n)(*[_ptr(t) for t in dk_accs]), (C.c_void_p * n)(*[_ptr(t) for t in dv_accs]),
+                        _ptr(dq), _ptr(dk), _ptr(dv))
+        _check(_lib.sppo_attn_bwd(self.h, C.byref(layout.c), chunk, _ptr(q), C.byref(kv), C.byref(args), flags,
+                                  _stream(stream)))
+
+    # -------------------------------------------------------------- host arena / copies
+    def host_alloc(self, nbytes: int) -> int:
+        p = C.c_void_p()
+        _check(_lib.sppo_host_alloc(self.h, nbytes, C.byref(p)))
+        return p.value
+
+    def host_free(self, ptr: int):
+        _check(_lib.sppo_host_free(self.h, ptr))
+
+    def kv_offload(self, chunk: int, dev, host: int, nbytes: int, alpha: float = 1.0, producer=None, done=None) -> int:
+        copied = C.c_size_t()
+        _check(_lib.sppo_kv_offload(self.h, chunk, _ptr(dev), host, nbytes, alpha, _stream(producer), _event(done),
+                                    C.byref(copied)))
+        return copied.value
+
+    def kv_prefetch(self, chunk: int, host: int, dev, nbytes: int, consumer=None, done=None):
+        _check(_lib.sppo_kv_prefetch(self.h, chunk, host, _ptr(dev), nbytes, _stream(consumer), _event(done)))
