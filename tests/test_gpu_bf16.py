@@ -1,0 +1,77 @@
+"""GPU parity of the bf16 tensor-core path (sm_100a tcgen05 kernels) against the
+fp64 oracle, element by element, on the same synth inputs (bf16-rounded values
+up-cast to fp64 on the oracle side).  Tolerances from north_star (reading L7):
+O: |gpu - ref| <= 2e-2 + 1e-2 |ref|;  dQ/dK/dV: 5e-2 + 5e-2 |ref|;
+LSE (unstated): 1e-3 absolute."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import make_inputs, ragged_offsets
+
+pytestmark = pytest.mark.gpu
+
+O_TOL = dict(atol=2e-2, rtol=1e-2)
+G_TOL = dict(atol=5e-2, rtol=5e-2)
+LSE_TOL = dict(atol=1e-3, rtol=0)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2503_10377_b200 import sppo
+    c = sppo.Context(0)
+    yield c
+    c.close()
+
+
+def make(S, h, seed):
+    x = make_inputs(S, range(h), 128, seed=seed, dtype=torch.bfloat16)
+    return x, {k: v.cuda() for k, v in x.items()}
+
+
+def fwd_only(ctx, S, h, offsets, seed=0, window=None):
+    from paper_2503_10377_b200 import engine, sppo
+    x, dev = make(S, h, seed)
+    L = sppo.Layout(h, 128, offsets, dtype=sppo.SPPO_BF16)
+    eng = engine.ChunkedAttention(ctx, L, window=window)
+    for i in range(L.num_chunks):
+        eng.forward_chunk(i, dev["q"], dev["k"], dev["v"])
+    torch.cuda.synchronize()
+    ctx.sync()
+    xn = {k: v.double().numpy() for k, v in x.items()}
+    return eng, xn
+
+
+@pytest.mark.parametrize("S,h,N,ragged", [(1024, 2, 4, False), (1000, 1, 3, True), (4096, 2, 4, False),
+                                          (777, 3, 5, True), (256, 1, 1, False), (130, 2, 2, True)])
+def test_bf16_forward_matches_oracle(ctx, S, h, N, ragged):
+    off = ragged_offsets(S, N, seed=S) if ragged else [i * S // N for i in range(N + 1)]
+    eng, xn = fwd_only(ctx, S, h, off, seed=S)
+    o, lse = oracle.causal_attention_dense(xn["q"], xn["k"], xn["v"])
+    got_o = eng.o.double().cpu().numpy()
+    got_lse = eng.lse_heads_major().double().cpu().numpy()
+    np.testing.assert_allclose(got_lse, lse, **LSE_TOL)
+    np.testing.assert_allclose(got_o, o, **O_TOL)
+    # tighter diagnostic: bf16 output rounding dominates (2^-8 relative)
+    assert np.abs(got_o - o).max() < 1.6e-2
+
+
+def test_bf16_forward_deterministic(ctx):
+    off = [0, 512, 1024, 1536, 2048]
+    eng1, _ = fwd_only(ctx, 2048, 2, off, seed=3)
+    o1 = eng1.o.clone()
+    eng2, _ = fwd_only(ctx, 2048, 2, off, seed=3)
+    assert torch.equal(o1, eng2.o)
+
+
+def test_bf16_forward_n_invariance(ctx):
+    """Same inputs, N = 1 vs N = 8: O agrees within bf16 rounding (L12)."""
+    S, h = 2048, 2
+    e1, _ = fwd_only(ctx, S, h, [0, S], seed=5)
+    e8, _ = fwd_only(ctx, S, h, [i * S // 8 for i in range(9)], seed=5)
+    d = (e1.o.float() - e8.o.float()).abs().max().item()
+    assert d < 2e-2
+    dl = (e1.lse_heads_major() - e8.lse_heads_major()).abs().max().item()
+    assert dl < 1e-3
