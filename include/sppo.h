@@ -175,15 +175,26 @@ sppo_status sppo_kv_offload(sppo_ctx ctx, int32_t chunk, const void* dev, void* 
                             size_t bytes, double alpha, void* producer, void* done,
                             size_t* copied);
 
+/* flags of sppo_kv_prefetch */
+enum {
+  SPPO_COPY_NO_ORDER = 1,   /* do not order the copy after `consumer`'s enqueued work */
+  SPPO_COPY_DEFER_WAIT = 2  /* do not make `consumer` wait; the caller waits on `done` */
+};
+
 /*
  * sppo_kv_prefetch — H2D copy of `bytes` from host back to `dev` on the ctx's
- * H2D copy stream, after all work already enqueued on `consumer` (so `dev` is
- * free), and makes `consumer` wait for the copy (resident "before the
- * backward propagation of the subsequence begins").  `done` (optional
- * cudaEvent_t) is recorded after the copy.
+ * H2D copy stream (offloaded activations must be resident "before the
+ * backward propagation of the subsequence begins").  By default (flags = 0)
+ * the copy starts after all work already enqueued on `consumer` (so `dev` is
+ * free) and `consumer` waits for the copy before any later work.
+ * SPPO_COPY_NO_ORDER drops the first ordering (dev known to be free);
+ * SPPO_COPY_DEFER_WAIT drops the second: the caller must make its stream wait
+ * on `done` (required then) before reading `dev` — this is how a copy is
+ * overlapped with compute enqueued after the call.  `done` (cudaEvent_t,
+ * optional otherwise) is recorded on the H2D stream after the copy.
  */
 sppo_status sppo_kv_prefetch(sppo_ctx ctx, int32_t chunk, const void* host, void* dev,
-                             size_t bytes, void* consumer, void* done);
+                             size_t bytes, void* consumer, void* done, int32_t flags);
 
 /* ---- host-side plan helpers ----------------------- */
 

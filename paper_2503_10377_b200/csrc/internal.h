@@ -77,10 +77,21 @@ struct Sm100Fwd {
   TmaSlots slots;
 };
 
+struct Sm100Bwd {
+  BwdParams p;
+  const void* desc_table;
+  int32_t q_slot, do_slot, dq_slot;  // bf16 Q_i, dO_i maps; fp32 dQ-accumulator map (reduce-add)
+  int32_t n;
+  int32_t start[kMaxWindow];
+  int32_t len[kMaxWindow];
+  int32_t tile_base[kMaxWindow + 1];  // prefix count of 128-key tiles per window chunk
+  TmaSlots slots;
+  float* dk[kMaxWindow];
+  float* dv[kMaxWindow];
+};
+
 cudaError_t launch_fwd_sm100(const Sm100Fwd& a, cudaStream_t s);
-cudaError_t launch_bwd_sm100(const BwdParams& p, const KvWindow& w, const KvGradWindow& g,
-                             const void* desc_table, const TmaSlots& slots, int32_t q_slot,
-                             int32_t do_slot, cudaStream_t s);
+cudaError_t launch_bwd_sm100(const Sm100Bwd& a, cudaStream_t s);
 
 // ---- elementwise helpers (bwd pre/post-processing, memory-bound) ---------
 // delta[h, r] = sum_d dO[r,h,d] * O[r,h,d]; optionally zero dq_acc.

@@ -65,16 +65,17 @@ EncodeTiledFn get_encode() {
 struct DescKey {
   const void* ptr;
   int64_t rows;
-  int32_t heads, d, box_rows;
+  int32_t heads, d, box_rows, elem;
   bool operator==(const DescKey& o) const {
-    return ptr == o.ptr && rows == o.rows && heads == o.heads && d == o.d && box_rows == o.box_rows;
+    return ptr == o.ptr && rows == o.rows && heads == o.heads && d == o.d && box_rows == o.box_rows &&
+           elem == o.elem;
   }
 };
 struct DescKeyHash {
   size_t operator()(const DescKey& k) const {
     size_t h = std::hash<const void*>()(k.ptr);
-    h ^= std::hash<int64_t>()(k.rows * 1000003 + k.heads * 131 + k.d * 7 + k.box_rows) + 0x9e3779b97f4a7c15ull +
-         (h << 6) + (h >> 2);
+    h ^= std::hash<int64_t>()(k.rows * 1000003 + k.heads * 131 + k.d * 7 + k.box_rows * 3 + k.elem) +
+         0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
     return h;
   }
 };
@@ -106,13 +107,14 @@ struct sppo_ctx_s {
 
 namespace {
 
-// Returns the descriptor slot for a token-major [rows, heads, d] bf16 tensor,
-// tiled as boxes of {64 elements of d (128 B, SWIZZLE_128B), 1 head, box_rows}.
+// Returns the descriptor slot for a token-major [rows, heads, d] tensor of
+// bf16 (elem = 2) or fp32 (elem = 4), tiled as boxes of {128 B of d
+// (SWIZZLE_128B), 1 head, box_rows}.
 // A new descriptor is staged in pinned memory and copied to the device table
 // on `stream` (stream-ordered before the kernel that uses it).
 sppo_status get_desc(sppo_ctx ctx, const void* ptr, int64_t rows, int heads, int d, int box_rows,
-                     cudaStream_t stream, int* slot) {
-  DescKey key{ptr, rows, heads, d, box_rows};
+                     cudaStream_t stream, int* slot, int elem = 2) {
+  DescKey key{ptr, rows, heads, d, box_rows, elem};
   auto it = ctx->desc_map.find(key);
   if (it != ctx->desc_map.end()) {
     *slot = it->second;
@@ -128,10 +130,10 @@ sppo_status get_desc(sppo_ctx ctx, const void* ptr, int64_t rows, int heads, int
   }
   const int s = ctx->desc_next++;
   cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)heads, (cuuint64_t)rows};
-  cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)heads * d * 2};
-  cuuint32_t box[3] = {64, 1, (cuuint32_t)box_rows};
+  cuuint64_t strides[2] = {(cuuint64_t)d * elem, (cuuint64_t)heads * d * elem};
+  cuuint32_t box[3] = {(cuuint32_t)(128 / elem), 1, (cuuint32_t)box_rows};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(&ctx->desc_host[s], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
+  CUresult r = enc(&ctx->desc_host[s], elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SPPO_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -425,18 +427,29 @@ sppo_status sppo_attn_bwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
   if (!bf16) {
     e = launch_bwd_simt_f32(p, w, g, strm);
   } else {
-    static TmaSlots slots;
-    int q_slot, do_slot;
-    if ((s = get_desc(ctx, q, p.q_len, p.heads, p.d, 128, strm, &q_slot))) return s;
-    if ((s = get_desc(ctx, a->dout, p.q_len, p.heads, p.d, 128, strm, &do_slot))) return s;
+    static Sm100Bwd sa;
+    sa.p = p;
+    sa.n = kv->n;
+    sa.desc_table = ctx->desc_dev;
+    if ((s = get_desc(ctx, q, p.q_len, p.heads, p.d, 128, strm, &sa.q_slot))) return s;
+    if ((s = get_desc(ctx, a->dout, p.q_len, p.heads, p.d, 128, strm, &sa.do_slot))) return s;
+    if ((s = get_desc(ctx, a->dq_acc, p.q_len, p.heads, p.d, 128, strm, &sa.dq_slot, 4))) return s;
+    int tiles = 0;
     for (int c = 0; c < kv->n; ++c) {
       int sk, sv;
       if ((s = get_desc(ctx, kv->k[c], w.len[c], p.heads, p.d, 128, strm, &sk))) return s;
       if ((s = get_desc(ctx, kv->v[c], w.len[c], p.heads, p.d, 128, strm, &sv))) return s;
-      slots.k[c] = (uint16_t)sk;
-      slots.v[c] = (uint16_t)sv;
+      sa.slots.k[c] = (uint16_t)sk;
+      sa.slots.v[c] = (uint16_t)sv;
+      sa.start[c] = w.start[c];
+      sa.len[c] = w.len[c];
+      sa.tile_base[c] = tiles;
+      tiles += (w.len[c] + 127) / 128;
+      sa.dk[c] = g.dk[c];
+      sa.dv[c] = g.dv[c];
     }
-    e = launch_bwd_sm100(p, w, g, ctx->desc_dev, slots, q_slot, do_slot, strm);
+    sa.tile_base[kv->n] = tiles;
+    e = launch_bwd_sm100(sa, strm);
   }
   if (e == cudaErrorNotSupported) return fail(SPPO_E_UNSUPPORTED, "this request is not implemented by the sm_100a kernels");
   if (e != cudaSuccess) return cuda_fail(e, "sppo_attn_bwd launch");
@@ -493,17 +506,23 @@ sppo_status sppo_kv_offload(sppo_ctx ctx, int32_t chunk, const void* dev, void* 
 }
 
 sppo_status sppo_kv_prefetch(sppo_ctx ctx, int32_t chunk, const void* host, void* dev, size_t bytes, void* consumer,
-                             void* done) {
+                             void* done, int32_t flags) {
   if (!ctx || !dev || !host) return fail(SPPO_E_ARG, "ctx/dev/host is NULL");
   if (chunk < 0) return fail(SPPO_E_ARG, "chunk < 0");
+  if (flags & ~(SPPO_COPY_NO_ORDER | SPPO_COPY_DEFER_WAIT)) return fail(SPPO_E_ARG, "unknown flags 0x%x", flags);
+  if ((flags & SPPO_COPY_DEFER_WAIT) && !done) return fail(SPPO_E_ARG, "SPPO_COPY_DEFER_WAIT needs a done event");
   SPPO_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
   std::lock_guard<std::mutex> lock(ctx->mu);
   cudaStream_t cons = (cudaStream_t)consumer;
-  SPPO_CUDA(cudaEventRecord(ctx->ev_cons, cons), "prefetch: record consumer");
-  SPPO_CUDA(cudaStreamWaitEvent(ctx->h2d, ctx->ev_cons, 0), "prefetch: wait consumer");
+  if (!(flags & SPPO_COPY_NO_ORDER)) {
+    SPPO_CUDA(cudaEventRecord(ctx->ev_cons, cons), "prefetch: record consumer");
+    SPPO_CUDA(cudaStreamWaitEvent(ctx->h2d, ctx->ev_cons, 0), "prefetch: wait consumer");
+  }
   if (bytes) SPPO_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->h2d), "prefetch: H2D copy");
-  SPPO_CUDA(cudaEventRecord(ctx->ev_copy, ctx->h2d), "prefetch: record copy");
-  SPPO_CUDA(cudaStreamWaitEvent(cons, ctx->ev_copy, 0), "prefetch: consumer wait");
+  if (!(flags & SPPO_COPY_DEFER_WAIT)) {
+    SPPO_CUDA(cudaEventRecord(ctx->ev_copy, ctx->h2d), "prefetch: record copy");
+    SPPO_CUDA(cudaStreamWaitEvent(cons, ctx->ev_copy, 0), "prefetch: consumer wait");
+  }
   if (done) SPPO_CUDA(cudaEventRecord((cudaEvent_t)done, ctx->h2d), "prefetch: record done");
   return SPPO_OK;
 }

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libsppo.so")
 
 SPPO_BF16, SPPO_FP32 = 0, 1
 SPPO_FIRST, SPPO_LAST = 1, 2
+SPPO_COPY_NO_ORDER, SPPO_COPY_DEFER_WAIT = 1, 2
 
 STATUS = {0: "SPPO_OK", 1: "SPPO_E_ARG", 2: "SPPO_E_SHAPE", 3: "SPPO_E_ALIGN", 4: "SPPO_E_STATE",
           5: "SPPO_E_NOT_RESIDENT", 6: "SPPO_E_OOM", 7: "SPPO_E_CUDA", 8: "SPPO_E_UNSUPPORTED"}
@@ -73,7 +74,7 @@ def _load():
         "sppo_host_alloc": ([vp, sz, C.POINTER(vp)], i32),
         "sppo_host_free": ([vp, vp], i32),
         "sppo_kv_offload": ([vp, i32, vp, vp, sz, C.c_double, vp, vp, C.POINTER(sz)], i32),
-        "sppo_kv_prefetch": ([vp, i32, vp, vp, sz, vp, vp], i32),
+        "sppo_kv_prefetch": ([vp, i32, vp, vp, sz, vp, vp, i32], i32),
         "sppo_partition_equal": ([C.c_int64, i32, C.POINTER(C.c_int64)], i32),
         "sppo_causal_pairs": ([C.POINTER(C.c_int64), i32, C.POINTER(C.c_int64)], i32),
         "sppo_offload_alpha": ([C.POINTER(C.c_double), i32, C.c_double, C.c_double, C.POINTER(C.c_double)], i32),
@@ -226,5 +227,5 @@ class Context:
                                     C.byref(copied)))
         return copied.value
 
-    def kv_prefetch(self, chunk: int, host: int, dev, nbytes: int, consumer=None, done=None):
-        _check(_lib.sppo_kv_prefetch(self.h, chunk, host, _ptr(dev), nbytes, _stream(consumer), _event(done)))
+    def kv_prefetch(self, chunk: int, host: int, dev, nbytes: int, consumer=None, done=None, flags: int = 0):
+        _check(_lib.sppo_kv_prefetch(self.h, chunk, host, _ptr(dev), nbytes, _stream(consumer), _event(done), flags))

@@ -75,3 +75,58 @@ def test_bf16_forward_n_invariance(ctx):
     assert d < 2e-2
     dl = (e1.lse_heads_major() - e8.lse_heads_major()).abs().max().item()
     assert dl < 1e-3
+
+
+def step(ctx, S, h, offsets, seed=0, bwd_window=None):
+    from paper_2503_10377_b200 import engine, sppo
+    x, dev = make(S, h, seed)
+    L = sppo.Layout(h, 128, offsets, dtype=sppo.SPPO_BF16)
+    eng = engine.ChunkedAttention(ctx, L)
+    N = L.num_chunks
+    eng.dk_acc.zero_()
+    eng.dv_acc.zero_()
+    for i in range(N):
+        eng.forward_chunk(i, dev["q"], dev["k"], dev["v"])
+    eng.window = bwd_window or 10**9
+    for i in range(N - 1, -1, -1):
+        eng.backward_chunk(i, dev["q"], dev["k"], dev["v"], dev["do"])
+    torch.cuda.synchronize()
+    ctx.sync()
+    xn = {k: v.double().numpy() for k, v in x.items()}
+    return eng, xn
+
+
+def check_grads(eng, xn):
+    ref = oracle.causal_attention_dense_bwd(xn["q"], xn["k"], xn["v"], xn["do"])
+    np.testing.assert_allclose(eng.o.double().cpu().numpy(), ref["o"], **O_TOL)
+    for key in ("dq", "dk", "dv"):
+        got = getattr(eng, key).double().cpu().numpy()
+        np.testing.assert_allclose(got, ref[key], **G_TOL, err_msg=key)
+    return ref
+
+
+@pytest.mark.parametrize("S,h,N,ragged", [(1024, 2, 4, False), (1000, 1, 3, True), (777, 3, 5, True),
+                                          (4096, 2, 4, False), (130, 2, 2, True), (256, 1, 1, False)])
+def test_bf16_backward_matches_oracle(ctx, S, h, N, ragged):
+    off = ragged_offsets(S, N, seed=S) if ragged else [i * S // N for i in range(N + 1)]
+    eng, xn = step(ctx, S, h, off, seed=S + 1)
+    check_grads(eng, xn)
+
+
+def test_bf16_backward_split_windows(ctx):
+    """Backward over windows of 2 prior chunks (dQ accumulates across launches,
+    dK_i/dV_i finalised by the window holding chunk i)."""
+    off = [0, 200, 512, 700, 1024, 1300]
+    eng, xn = step(ctx, 1300, 2, off, seed=9, bwd_window=2)
+    check_grads(eng, xn)
+
+
+def test_bf16_gradient_identities(ctx):
+    """sum_t dK_t = 0 and sum_t dV_t = sum_p dO_p (oracle pins, checked on the GPU result)."""
+    off = [i * 2048 // 4 for i in range(5)]
+    eng, xn = step(ctx, 2048, 2, off, seed=4)
+    dk = eng.dk.double().sum(0).cpu().numpy()   # final bf16 dK (all chunks)
+    dv = eng.dv.double().sum(0).cpu().numpy()
+    scale = np.abs(eng.dk.double().cpu().numpy()).sum(0).max()
+    assert np.abs(dk).max() < 1e-2 * scale
+    np.testing.assert_allclose(dv, xn["do"].sum(0), atol=0.3, rtol=1e-2)
