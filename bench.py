@@ -1,0 +1,365 @@
+"""Benchmark of the SPPO hot path on B200: chunked causal attention fwd+bwd.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One step = one pass of the whole hot path over one synthetic batch: partition
+(a0) -> forward of chunks 0..N-1 (a1) -> backward of chunks N-1..0 (a5-a7),
+all through the C ABI (libsppo.so).  Workload at N=1: configs[1] (C2, GPT-7B
+attention layer: h=32, d=128, S=128K, 16 chunks).  For N>1 (torchrun) the
+heads are sharded over the ranks (Ulysses-style head parallelism without the
+all-to-all); no collective inside the step; one NCCL all-gather
+of O after timing (not timed).  Rank 0 prints one JSON line.
+
+FLOP convention: 4d per causal pair forward, 10d backward.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+CONFIGS = {
+    "C1": dict(heads=1, d=64, S=1024, N=4, dtype="fp32",
+               workload="configs[0] tiny: 1 head, d=64, S=1024, N=4, fp32"),
+    "C2": dict(heads=32, d=128, S=131072, N=16, dtype="bf16",
+               workload="configs[1] GPT-7B attention layer: 32 heads, d=128, S=128K, N=16, bf16"),
+    "C3": dict(heads=32, d=128, S=1048576, N=64, dtype="bf16",
+               workload="configs[2] GPT-7B shape: 32 heads, d=128, S=1M, N=64, bf16"),
+    "C4": dict(heads=40, d=128, S=524288, N=32, dtype="bf16",
+               workload="configs[3] GPT-13B shape: 40 heads, d=128, S=512K, N=32, bf16"),
+}
+METRIC = "chunked attn fwd+bwd TFLOP/s per B200 (% BF16 peak), tokens/s at 1/2/4/8 GPU"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(burst=d.get("bf16_tflops", 1590.0), sustained=d.get("bf16_tflops_sustained", 1400.0),
+                    hbm=d.get("hbm_gbs", 6650.0), source="MEASURED_PEAKS.json (measured)")
+    return dict(burst=1590.0, sustained=1400.0, hbm=6650.0, source="B200_PROFILING.md fallback")
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) > 8 and r[1].strip().replace(".", "").isdigit()]
+        if not sm:
+            return None
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[5:9]):
+                if v.strip() == "Active":
+                    reasons.add(n)
+        load = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": float(rows[0][2]), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(float(r[3]) for r in rows if r[3].strip()[:1].isdigit())}
+
+
+def flops_of(offsets, heads, d, part="fwd+bwd"):
+    from paper_2503_10377_b200 import sppo
+    pairs = sppo.causal_pairs(offsets)  # product's own host helper (a0 / FLOP accounting)
+    per = {"fwd": 4, "bwd": 10, "fwd+bwd": 14}[part] * d
+    return heads * per * pairs
+
+
+# ------------------------------------------------------------------ CPU baseline (oracle)
+def cpu_oracle_sample(seconds_target=12.0):
+    """The fp64 oracle as it stands, on a bounded sample of the C2 workload: one
+    head, the first S_s tokens as 2 chunks of C2's 8192-token chunk length.
+    Returns dict(value TFLOP/s, cores, sample, seconds)."""
+    import numpy as np
+
+    import oracle
+    from synth import make_inputs
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([t.get("num_threads", 1) for t in threadpool_info()] or [1])
+    except Exception:
+        cores = os.cpu_count()
+    S_s, N_s = 16384, 2
+    x = make_inputs(S_s, [0], 128, seed=0, dtype=torch.bfloat16)
+    xn = {k: v.double().numpy() for k, v in x.items()}
+    off = [0, 8192, 16384]
+    t0 = time.perf_counter()
+    o, lse = oracle.chunked_attention_fwd(xn["q"], xn["k"], xn["v"], off)
+    oracle.chunked_attention_bwd(xn["q"], xn["k"], xn["v"], o, lse, xn["do"], off)
+    dt = time.perf_counter() - t0
+    fl = 14 * 128 * (S_s * (S_s + 1) // 2)
+    return dict(value=fl / dt / 1e12, cores=int(cores), seconds=dt,
+                sample=f"oracle fp64 chunked fwd+bwd, 1 head x {S_s} tokens in {N_s} chunks of 8192 (C2 chunk length), "
+                       f"{fl:.3e} FLOP in {dt:.1f}s")
+
+
+# ------------------------------------------------------------------ distributed
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def head_range(heads, ws, rank):
+    if heads % ws:
+        raise SystemExit(f"heads={heads} not divisible by {ws} GPUs")
+    per = heads // ws
+    return list(range(rank * per, (rank + 1) * per))
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ our implementation
+def run_ours(args, cfg, ws, rank, local):
+    from paper_2503_10377_b200 import engine, sppo
+    from synth import make_tensor
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    heads = head_range(cfg["heads"], ws, rank)
+    h, d, S, N = len(heads), cfg["d"], cfg["S"], cfg["N"]
+    dtype = sppo.SPPO_BF16 if cfg["dtype"] == "bf16" else sppo.SPPO_FP32
+    tdt = torch.bfloat16 if dtype == sppo.SPPO_BF16 else torch.float32
+    ctx = sppo.Context(local)
+    offsets = sppo.partition_equal(S, N)  # a0, in the product's C helper
+    L = sppo.Layout(h, d, offsets, dtype=dtype)
+    x = {t: make_tensor(t, S, heads, d, seed=0, dtype=tdt, device=dev) for t in ("q", "k", "v", "do")}
+    eng = engine.ChunkedAttention(ctx, L, device=dev, timing=True)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        eng.step(x["q"], x["k"], x["v"], x["do"], stream)
+    torch.cuda.synchronize()
+    eng.events = {"fwd": [], "bwd": []}
+    eng.launches = 0
+    barrier(ws)
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        eng.step(x["q"], x["k"], x["v"], x["do"], stream)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    barrier(ws)
+    ms_local = t0.elapsed_time(t1) / args.steps
+    ms = max_over_ranks(ms_local, ws)
+    launches = eng.launches // args.steps
+    fwd_ms = eng.kernel_ms("fwd") / args.steps
+    bwd_ms = eng.kernel_ms("bwd") / args.steps
+
+    fl_dev = flops_of(offsets, h, d)
+    fl_total = flops_of(offsets, cfg["heads"], d)
+    peaks = load_peaks()
+    tflops = fl_total / (ms * 1e-3) / 1e12
+    per_gpu = tflops / ws
+    bwd_fl = flops_of(offsets, h, d, "bwd")
+    fwd_fl = flops_of(offsets, h, d, "fwd")
+    ach_bwd = bwd_fl / (bwd_ms * 1e-3) / 1e12
+    ach_fwd = fwd_fl / (fwd_ms * 1e-3) / 1e12
+
+    # ---- end to end through host buffers (pinned), same metric
+    e2e = None
+    if not args.no_e2e:
+        nb = S * h * d * eng.elem
+        host_in = {t: ctx.host_alloc(nb) for t in ("q", "k", "v", "do")}
+        host_out = {t: ctx.host_alloc(nb) for t in ("o", "dq", "dk", "dv")}
+        for t in ("q", "k", "v", "do"):  # stage the synthetic inputs in host memory once (outside timing)
+            ctx.kv_offload(0, x[t], host_in[t], nb, 1.0, producer=stream)
+        ctx.sync()
+        res = []
+        for rep in range(1 + max(1, args.steps // 2)):
+            torch.cuda.synchronize()
+            barrier(ws)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            h2d, d2h, last = eng.step_host_io(host_in, host_out, x, stream)
+            # end of step = the last D2H of a result has landed in host memory
+            e1 = torch.cuda.Event(enable_timing=True)
+            stream.wait_event(last)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if rep > 0:  # first rep is a warm-up
+                res.append(e0.elapsed_time(e1))
+        e2e_ms = max_over_ranks(statistics.median(res), ws)
+        e2e = {"value": round(fl_total / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+               "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d * ws, "d2h_bytes_per_step": d2h * ws,
+               "path": "pinned host Q,K,V,dO -> chunk-wise sppo_kv_prefetch overlapped with compute; "
+                       "O, dQ, dK, dV -> sppo_kv_offload after each chunk"}
+        for p in list(host_in.values()) + list(host_out.values()):
+            ctx.host_free(p)
+
+    # ---- Type-1 offload policy (alpha) : exposed offload time vs resident
+    offload = None
+    if not args.no_offload:
+        bw = 56e9  # pinned D2H GB/s measured on this pool (tools/box_probe.py, gpurun_out/box_probe.json)
+        eng.events = {"fwd": [], "bwd": []}
+        eng.step(x["q"], x["k"], x["v"], x["do"], stream)
+        torch.cuda.synchronize()
+        t_fwd = [a.elapsed_time(b) * 1e-3 for a, b in eng.events["fwd"]]
+        A = [eng.type1_bytes(i) for i in range(N)]
+        thr = [bw * (t_fwd[i + 1] if i + 1 < N else 0.0) for i in range(N)]
+        alpha = sppo.offload_alpha(A, thr, 0.0)
+        eng.timing = False
+        res = []
+        moved = None
+        for rep in range(1 + max(1, args.steps // 2)):
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            moved = eng.step_offload(x["q"], x["k"], x["v"], x["do"], alpha, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if rep > 0:
+                res.append(e0.elapsed_time(e1))
+        off_ms = max_over_ranks(statistics.median(res), ws)
+        offload = {"policy": "type1-alpha (Q,O,LSE offloaded after fwd(i), prefetched depth 2 before bwd(i))",
+                   "ms_per_step": round(off_ms, 3), "resident_ms_per_step": round(ms, 3),
+                   "exposed_pct": round(100.0 * (off_ms - ms) / ms, 2),
+                   "d2h_bytes": moved["d2h"], "h2d_bytes": moved["h2d"],
+                   "alpha": [round(a, 3) for a in alpha], "bw_d2h_gbs_assumed": bw / 1e9}
+        eng.free_host()
+
+    # ---- final gather of O over NCCL (multi-GPU only, not timed in value)
+    gather = None
+    if ws > 1:
+        import torch.distributed as dist
+        out = torch.empty((ws,) + tuple(eng.o.shape), dtype=eng.o.dtype, device=dev)
+        g0 = time.perf_counter()
+        dist.all_gather_into_tensor(out, eng.o.contiguous())
+        torch.cuda.synchronize()
+        gather = {"op": "all_gather_into_tensor(O) over NCCL", "ms": round((time.perf_counter() - g0) * 1e3, 2),
+                  "bytes": out.numel() * out.element_size()}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        c = cpu_oracle_sample()
+        cpu = {"value": round(c["value"], 6), "unit": "TFLOP/s", "cores": c["cores"], "kind": "oracle",
+               "sample": c["sample"]}
+
+    ctx.close()
+    if rank != 0:
+        return None
+    line = {
+        "metric": METRIC, "value": round(tflops, 2), "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+        "config": {"workload": cfg["workload"], "heads": cfg["heads"], "heads_per_gpu": h, "head_dim": d,
+                   "seq_len": S, "chunks": N, "chunk_len": S // N, "policy": "resident (KV + activations on GPU)",
+                   "parallelism": f"heads sharded over {ws} GPU(s), no collective in step",
+                   "l2": f"inputs {4 * S * h * d * eng.elem / 2**30:.1f} GiB per GPU > 126 MB L2 (no flush needed)"},
+        "per_gpu_tflops": round(per_gpu, 2),
+        "pct_bf16_peak": {"burst": round(100 * per_gpu / peaks["burst"], 1),
+                          "sustained": round(100 * per_gpu / peaks["sustained"], 1),
+                          "datasheet_2250": round(100 * per_gpu / 2250.0, 1), "source": peaks["source"]},
+        "tokens_per_s": round(S / (ms * 1e-3), 1), "tgs": round(S / (ms * 1e-3) / ws, 1),
+        "fwd_tflops": round(ach_fwd, 2), "bwd_tflops": round(ach_bwd, 2),
+        "roofline": {"bound": "tensor", "kernel": "bwd_kernel (sppo_attn_bwd calls, incl. Delta/cast helpers)",
+                     "achieved": round(ach_bwd, 2), "peak": peaks["sustained"], "unit": "TFLOP/s",
+                     "frac": round(ach_bwd / peaks["sustained"], 3), "traffic": None,
+                     "peak_kind": "sustained bf16 (kernel timed inside a long step), " + peaks["source"],
+                     "share_of_step": round(bwd_ms / ms, 3)},
+        "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "offload": offload, "gather": gather,
+        "cpu_baseline": cpu,
+    }
+    return line
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+def run_reference(args, cfg, ws, rank):
+    if rank != 0:
+        return None
+    res = []
+    c = None
+    for it in range(args.warmup + args.steps):
+        c = cpu_oracle_sample()
+        if it >= args.warmup:
+            res.append(c)
+    secs = statistics.median([r["seconds"] for r in res])
+    val = statistics.median([r["value"] for r in res])
+    return {"metric": METRIC, "value": round(val, 6), "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(secs * 1e3, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": cfg["workload"] + " -- bounded oracle sample per step", "sample": c["sample"]},
+            "cpu_baseline": {"value": round(val, 6), "unit": "TFLOP/s", "cores": c["cores"], "kind": "oracle",
+                             "sample": c["sample"]},
+            "e2e": {"value": round(val, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-offload", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: warmup < 3 violates the timing rules", file=sys.stderr)
+    ws, rank, local = dist_setup()
+    cfg = CONFIGS[args.config]
+    line = run_reference(args, cfg, ws, rank) if args.impl == "reference" else run_ours(args, cfg, ws, rank, local)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

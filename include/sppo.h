@@ -202,9 +202,12 @@ sppo_status sppo_kv_prefetch(sppo_ctx ctx, int32_t chunk, const void* host, void
 sppo_status sppo_partition_equal(int64_t S, int32_t N, int64_t* offsets_out);
 /* Causal (q,k) pairs of all chunks: sum_i s_i c_i + s_i (s_i + 1) / 2. */
 sppo_status sppo_causal_pairs(const int64_t* offsets, int32_t N, int64_t* pairs_out);
-/* alpha_i = min(1, m_threshold / A_i) for i < N-1, alpha_{N-1} = last,
- * A_i <= 0 => alpha_i = 1 (reading L9). */
-sppo_status sppo_offload_alpha(const double* A, int32_t N, double m_threshold, double last,
+/* Sequence-aware offload ratio (P:371-377 [§5.2]; reading L9):
+ * alpha_i = min(1, M_i / A_i) for i < N-1 with M_i = m_threshold[i] (the bytes
+ * the D2H link moves during the compute that the offload of chunk i overlaps,
+ * BW_D2H * T_comp(i+1); the paper's single M_threshold is the constant case),
+ * alpha_{N-1} = last, A_i <= 0 => alpha_i = 1.  m_threshold has N entries. */
+sppo_status sppo_offload_alpha(const double* A, const double* m_threshold, int32_t N, double last,
                                double* alpha_out);
 
 #ifdef __cplusplus

@@ -57,13 +57,16 @@ def offsets_from_lengths(lengths):
     return out
 
 
-def offload_alpha(A, m_threshold: float, last: float = 1.0):
+def offload_alpha(A, m_threshold, last: float = 1.0):
     """alpha_i = min(1, M_threshold / A_i) for i < last chunk (P:377, S:241);
     A_i = 0 gives alpha_i = 1 (nothing to offload).  The last chunk's
     ratio is ``last``: 1.0 per the paper ("alpha_k = 1 for final
     subsequence"), 0.0 in the single-layer bench (reading L9: its backward
-    consumes it immediately)."""
+    consumes it immediately).  ``m_threshold`` is the paper's constant
+    M_threshold, or a per-chunk list M_i = BW_D2H * T_comp(i+1) (reading L9,
+    "sequence-aware": the offload of i overlaps the compute of i+1)."""
     n = len(A)
+    thr = list(m_threshold) if hasattr(m_threshold, "__len__") else [m_threshold] * n
     out = []
     for i, a in enumerate(A):
         if i == n - 1:
@@ -71,7 +74,7 @@ def offload_alpha(A, m_threshold: float, last: float = 1.0):
         elif a <= 0:
             out.append(1.0)
         else:
-            out.append(min(1.0, float(m_threshold) / float(a)))
+            out.append(min(1.0, float(thr[i]) / float(a)))
     return out
 
 

@@ -550,18 +550,19 @@ sppo_status sppo_causal_pairs(const int64_t* off, int32_t N, int64_t* pairs) {
   return SPPO_OK;
 }
 
-sppo_status sppo_offload_alpha(const double* A, int32_t N, double m_threshold, double last, double* alpha) {
-  if (!A || !alpha) return fail(SPPO_E_ARG, "NULL argument");
+sppo_status sppo_offload_alpha(const double* A, const double* m_threshold, int32_t N, double last, double* alpha) {
+  if (!A || !m_threshold || !alpha) return fail(SPPO_E_ARG, "NULL argument");
   if (N < 1) return fail(SPPO_E_SHAPE, "N < 1");
-  if (!(m_threshold >= 0.0)) return fail(SPPO_E_ARG, "m_threshold < 0");
   if (!(last >= 0.0 && last <= 1.0)) return fail(SPPO_E_ARG, "last alpha not in [0,1]");
+  for (int32_t i = 0; i < N; ++i)
+    if (!(m_threshold[i] >= 0.0)) return fail(SPPO_E_ARG, "m_threshold[%d] < 0", i);
   for (int32_t i = 0; i < N; ++i) {
     if (i == N - 1)
       alpha[i] = last;
     else if (A[i] <= 0.0)
       alpha[i] = 1.0;
     else
-      alpha[i] = fmin(1.0, m_threshold / A[i]);
+      alpha[i] = fmin(1.0, m_threshold[i] / A[i]);
   }
   return SPPO_OK;
 }

@@ -3,8 +3,18 @@
 One step = forward over chunks i = 0..N-1 (ascending) then backward over
 i = N-1..0 (reading L11), each chunk's prior-KV set 0..i visited in windows of
 at most ``window`` chunks (FIRST/LAST carry).  Every compute
-step is a call into libsppo (sppo_attn_fwd / sppo_attn_bwd); this module only
-allocates buffers (torch, device memory) and sequences the calls.
+step is a call into libsppo (sppo_attn_fwd / sppo_attn_bwd) and every copy a
+call to sppo_kv_offload / sppo_kv_prefetch; this module only allocates buffers
+(torch device memory, pinned host memory from sppo_host_alloc) and sequences
+the calls.
+
+Two-level activation management (P:356 [§5.1], P:369-377 [§5.2]):
+  * level 1 (GPU): K_j, V_j of every chunk stay resident (Type-0, P:356);
+  * level 2 (host): the Type-1 tensors of chunk i (Q_i, O_i, LSE_i — used once
+    in forward, once in backward) are offloaded with ratio alpha_i right after
+    fwd(i) on the D2H stream, overlapping fwd(i+1), and prefetched on
+    the H2D stream before bwd(i), at most ``depth`` chunks ahead.
+    alpha_i = min(1, BW_D2H * T_fwd(i+1) / A_i), alpha_{N-1} = 0 (reading L9).
 
 Buffer layout in HBM: full-sequence token-major tensors
 [S, h, d] whose chunk i is the contiguous row range [c_i, c_{i+1}); LSE stored
@@ -23,14 +33,19 @@ DTYPES = {sppo.SPPO_BF16: torch.bfloat16, sppo.SPPO_FP32: torch.float32}
 
 
 class ChunkedAttention:
-    def __init__(self, ctx: sppo.Context, layout: sppo.Layout, device="cuda", window: int | None = None):
+    def __init__(self, ctx: sppo.Context, layout: sppo.Layout, device="cuda", window: int | None = None,
+                 timing: bool = False):
         self.ctx, self.L = ctx, layout
         self.device = torch.device(device)
         self.window = window if window else 10**9
+        self.timing = timing
+        self.launches = 0
+        self.events = {"fwd": [], "bwd": []}
         h, d = layout.heads, layout.head_dim
         S = layout.offsets[-1]
         smax = max(layout.chunk_len(i) for i in range(layout.num_chunks))
         dt = DTYPES[layout.dtype]
+        self.elem = torch.tensor([], dtype=dt).element_size()
         f32 = dict(dtype=torch.float32, device=self.device)
         self.S = S
         self.o = torch.empty((S, h, d), dtype=dt, device=self.device)
@@ -45,6 +60,7 @@ class ChunkedAttention:
         self.o_acc = torch.empty((smax, h, d), **f32)
         self.m = torch.empty((smax * h,), **f32)
         self.l = torch.empty((smax * h,), **f32)
+        self._host = {}
 
     # chunk views -----------------------------------------------------------
     def rows(self, t, i):
@@ -61,25 +77,44 @@ class ChunkedAttention:
         w = self.window
         return [ids[a:a + w] for a in range(0, len(ids), w)]
 
-    # one step ----------------------------------------------------------------
+    def _ev(self, kind, stream):
+        if not self.timing:
+            return None
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        self.events[kind].append((e0, e1))
+        return e1
+
+    def kernel_ms(self, kind):
+        """Sum of CUDA-event durations of the recorded calls (after a sync)."""
+        return sum(a.elapsed_time(b) for a, b in self.events[kind])
+
+    # forward / backward of one chunk ----------------------------------------
     def forward_chunk(self, i, q, k, v, stream=None):
         L = self.L
         s = L.chunk_len(i)
         h = L.heads
         wins = self.windows(i)
         state = (self.o_acc[:s], self.m[:s * h], self.l[:s * h])
+        strm = stream or torch.cuda.current_stream()
+        end = self._ev("fwd", strm)
         for n, ids in enumerate(wins):
             flags = (sppo.SPPO_FIRST if n == 0 else 0) | (sppo.SPPO_LAST if n == len(wins) - 1 else 0)
             self.ctx.attn_fwd(L, i, self.rows(q, i), ids, [self.rows(k, j) for j in ids],
                               [self.rows(v, j) for j in ids], flags=flags,
                               state=None if len(wins) == 1 else state,
-                              o=self.rows(self.o, i), lse=self.lse_view(i), stream=stream)
+                              o=self.rows(self.o, i), lse=self.lse_view(i), stream=strm)
+            self.launches += 1
+        if end is not None:
+            end.record(strm)
 
     def backward_chunk(self, i, q, k, v, do, stream=None):
         L = self.L
         s = L.chunk_len(i)
         h = L.heads
         wins = self.windows(i)
+        strm = stream or torch.cuda.current_stream()
+        end = self._ev("bwd", strm)
         for n, ids in enumerate(wins):
             flags = (sppo.SPPO_FIRST if n == 0 else 0) | (sppo.SPPO_LAST if n == len(wins) - 1 else 0)
             has_i = i in ids
@@ -88,8 +123,13 @@ class ChunkedAttention:
                               self.rows(do, i), self.delta[:s * h], self.dq_acc[:s],
                               [self.rows(self.dk_acc, j) for j in ids], [self.rows(self.dv_acc, j) for j in ids],
                               dq=self.rows(self.dq, i), dk=self.rows(self.dk, i) if has_i else None,
-                              dv=self.rows(self.dv, i) if has_i else None, flags=flags, stream=stream)
+                              dv=self.rows(self.dv, i) if has_i else None, flags=flags, stream=strm)
+            # main kernel + Delta preprocess on FIRST + dQ cast on LAST
+            self.launches += 1 + (flags & sppo.SPPO_FIRST != 0) + (flags & sppo.SPPO_LAST != 0)
+        if end is not None:
+            end.record(strm)
 
+    # one step, all activations resident ---------------------------------------
     def step(self, q, k, v, do, stream=None):
         """Full forward + backward over all chunks (resident policy)."""
         N = self.L.num_chunks
@@ -100,6 +140,126 @@ class ChunkedAttention:
         for i in range(N - 1, -1, -1):
             self.backward_chunk(i, q, k, v, do, stream)
         return dict(o=self.o, lse=self.lse, dq=self.dq, dk=self.dk, dv=self.dv)
+
+    # one step with Type-1 offload (two-level activation management) ----------
+    def type1_bytes(self, i):
+        """A_i: bytes of chunk i's Type-1 tensors (Q_i, O_i, LSE_i)."""
+        s, h, d = self.L.chunk_len(i), self.L.heads, self.L.head_dim
+        return 2 * s * h * d * self.elem + 4 * s * h
+
+    def _host_buf(self, key, nbytes):
+        if key not in self._host:
+            self._host[key] = (self.ctx.host_alloc(nbytes), nbytes)
+        return self._host[key][0]
+
+    def free_host(self):
+        for ptr, _ in self._host.values():
+            self.ctx.host_free(ptr)
+        self._host.clear()
+
+    def step_offload(self, q, k, v, do, alpha, stream=None, depth: int = 2, poison: bool = False):
+        """Forward + backward where Q_i, O_i and LSE_i leave the GPU after fwd(i)
+        (alpha_i-prefix of each token-major buffer, LSE whole when alpha_i > 0)
+        and come back before bwd(i).  With ``poison`` the device copies are
+        overwritten with NaN after the offload completes, proving that the
+        backward reads the prefetched bytes.  Returns copy statistics."""
+        L = self.L
+        N = L.num_chunks
+        strm = stream or torch.cuda.current_stream()
+        self.dk_acc.zero_()
+        self.dv_acc.zero_()
+        moved = {"d2h": 0, "h2d": 0}
+        plan = {}
+        done = {}
+        for i in range(N):
+            self.forward_chunk(i, q, k, v, strm)
+            a = float(alpha[i])
+            if a <= 0.0:
+                continue
+            parts = []
+            for name, t in (("q", self.rows(q, i)), ("o", self.rows(self.o, i)), ("lse", self.lse_view(i))):
+                nb = t.numel() * t.element_size()
+                host = self._host_buf((name, i), nb)
+                ev = torch.cuda.Event()
+                n = self.ctx.kv_offload(i, t, host, nb, alpha=(a if name != "lse" else 1.0), producer=strm,
+                                        done=ev)
+                moved["d2h"] += n
+                parts.append((name, t, host, n, ev))
+            plan[i] = parts
+            if poison:
+                for _, t, _, n, ev in parts:
+                    strm.wait_event(ev)
+                    t.view(torch.uint8)[:n].fill_(0xFF)  # NaN pattern in bf16/fp32
+        issued = set()
+
+        def prefetch(i):
+            if i < 0 or i in issued or i not in plan:
+                return
+            issued.add(i)
+            evs = []
+            for name, t, host, n, ev in plan[i]:
+                # bytes must have reached the host first (D2H of the offload)
+                strm.wait_event(ev)
+                pe = torch.cuda.Event()
+                self.ctx.kv_prefetch(i, host, t, n, consumer=strm, done=pe,
+                                     flags=sppo.SPPO_COPY_DEFER_WAIT)
+                moved["h2d"] += n
+                evs.append(pe)
+            done[i] = evs
+
+        for i in range(N - 1, -1, -1):
+            for dd in range(depth):
+                prefetch(i - dd)
+            for pe in done.get(i, []):
+                strm.wait_event(pe)
+            self.backward_chunk(i, q, k, v, do, strm)
+        return moved
+
+    # end-to-end step through host buffers --------------------------------------
+    def step_host_io(self, host_in, host_out, dev_in, stream=None):
+        """One step whose inputs start in pinned host memory and whose results end
+        there: chunk-wise H2D of Q_i, K_i, V_i, dO_i (sppo_kv_prefetch, deferred
+        wait) overlapped with compute, D2H of O_i after fwd(i) and of dQ_i, dK_i,
+        dV_i after bwd(i) (sppo_kv_offload).  Returns (h2d_bytes, d2h_bytes,
+        last_done_event)."""
+        L = self.L
+        N = L.num_chunks
+        strm = stream or torch.cuda.current_stream()
+        h2d = d2h = 0
+        ready = []
+        for i in range(N):
+            evs = []
+            for name in ("q", "k", "v", "do"):
+                t = self.rows(dev_in[name], i)
+                nb = t.numel() * t.element_size()
+                off = L.offsets[i] * L.heads * L.head_dim * self.elem
+                ev = torch.cuda.Event()
+                self.ctx.kv_prefetch(i, host_in[name] + off, t, nb, consumer=strm, done=ev,
+                                     flags=sppo.SPPO_COPY_NO_ORDER | sppo.SPPO_COPY_DEFER_WAIT)
+                h2d += nb
+                evs.append(ev)
+            ready.append(evs)
+        self.dk_acc.zero_()
+        self.dv_acc.zero_()
+        last = None
+        for i in range(N):
+            for ev in ready[i][:3]:
+                strm.wait_event(ev)
+            self.forward_chunk(i, dev_in["q"], dev_in["k"], dev_in["v"], strm)
+            t = self.rows(self.o, i)
+            nb = t.numel() * t.element_size()
+            off = L.offsets[i] * L.heads * L.head_dim * self.elem
+            last = torch.cuda.Event()
+            d2h += self.ctx.kv_offload(i, t, host_out["o"] + off, nb, 1.0, producer=strm, done=last)
+        for i in range(N - 1, -1, -1):
+            strm.wait_event(ready[i][3])
+            self.backward_chunk(i, dev_in["q"], dev_in["k"], dev_in["v"], dev_in["do"], strm)
+            for name, t in (("dq", self.rows(self.dq, i)), ("dk", self.rows(self.dk, i)), ("dv", self.rows(self.dv, i))):
+                nb = t.numel() * t.element_size()
+                off = L.offsets[i] * L.heads * L.head_dim * self.elem
+                last = torch.cuda.Event()
+                d2h += self.ctx.kv_offload(i, t, host_out[name] + off, nb, 1.0, producer=strm, done=last)
+        return h2d, d2h, last
 
     def lse_heads_major(self):
         """[h, S] view assembled from per-chunk [h, s_i] blocks (for checks)."""

@@ -77,7 +77,8 @@ def _load():
         "sppo_kv_prefetch": ([vp, i32, vp, vp, sz, vp, vp, i32], i32),
         "sppo_partition_equal": ([C.c_int64, i32, C.POINTER(C.c_int64)], i32),
         "sppo_causal_pairs": ([C.POINTER(C.c_int64), i32, C.POINTER(C.c_int64)], i32),
-        "sppo_offload_alpha": ([C.POINTER(C.c_double), i32, C.c_double, C.c_double, C.POINTER(C.c_double)], i32),
+        "sppo_offload_alpha": ([C.POINTER(C.c_double), C.POINTER(C.c_double), i32, C.c_double,
+                                C.POINTER(C.c_double)], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -139,11 +140,14 @@ def causal_pairs(offsets) -> int:
     return out.value
 
 
-def offload_alpha(A, m_threshold: float, last: float = 1.0):
+def offload_alpha(A, m_threshold, last: float = 1.0):
+    """m_threshold: scalar (the paper's constant M_threshold) or per-chunk list."""
     n = len(A)
+    thr = list(m_threshold) if hasattr(m_threshold, "__len__") else [m_threshold] * n
     a = (C.c_double * n)(*A)
+    m = (C.c_double * n)(*thr)
     out = (C.c_double * n)()
-    _check(_lib.sppo_offload_alpha(a, n, m_threshold, last, out))
+    _check(_lib.sppo_offload_alpha(a, m, n, last, out))
     return list(out)
 
 

@@ -47,6 +47,8 @@ def test_offload_alpha_matches_oracle():
         assert sppo.offload_alpha(A, m, last) == pytest.approx(oracle.offload_alpha(A, m, last), abs=0, rel=1e-15)
     with pytest.raises(sppo.SppoError):
         sppo.offload_alpha([1.0], 1.0, 2.0)
+    A, thr = [8.0, 6.0, 4.0, 2.0], [2.0, 3.0, 8.0, 1.0]
+    assert sppo.offload_alpha(A, thr, 0.0) == oracle.offload_alpha(A, thr, 0.0) == [0.25, 0.5, 1.0, 0.0]
 
 
 def test_ctx_without_gpu_fails_loudly():
