@@ -68,15 +68,6 @@ __device__ __forceinline__ uint32_t sw128(int r, int byte_in_row) {
   return lin ^ (((lin >> 7) & 7u) << 4);
 }
 
-template <uint32_t N>
-__device__ __forceinline__ void setmaxnreg_inc() {
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
-}
-template <uint32_t N>
-__device__ __forceinline__ void setmaxnreg_dec() {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
-}
-
 __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant__ Sm100Bwd a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   Bars& bars = *reinterpret_cast<Bars*>(smem + kOffBars);
@@ -126,7 +117,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant_
   const uint32_t tS = tmem, tdV = tmem + 128, tdP = tmem + 256, tdK = tmem + 384;
 
   if (warp >= 12) {
-    setmaxnreg_dec<96>();
+    setmaxnreg_dec<104>();
     if (warp == 13) {
       // ===================== TMA producer (+ LSE / Delta vectors) =====================
       const CUtensorMap* mq = tmap(a, a.q_slot);
@@ -151,10 +142,15 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant_
           tma_load_3d(smem + kOffQ + s * kTile, mq, &bars.q_full[s], 0, head, q0);
           tma_load_3d(smem + kOffQ + s * kTile + kHalf, mq, &bars.q_full[s], 64, head, q0);
         }
+        {
+          float4 w;
+          float* wp = reinterpret_cast<float*>(&w);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int r = q0 + lane * 4 + k;
-          sLSE[s * 128 + lane * 4 + k] = r < p.q_len ? lse_h[r] * kLog2e : INFINITY;  // OOB row -> P = 0
+          for (int k = 0; k < 4; ++k) {
+            const int r = q0 + lane * 4 + k;
+            wp[k] = r < p.q_len ? lse_h[r] * kLog2e : INFINITY;  // OOB row -> P = 0
+          }
+          *reinterpret_cast<float4*>(sLSE + s * 128 + lane * 4) = w;  // one conflict-free STS.128
         }
         mbar_arrive(&bars.q_full[s]);
         mbar_wait(&bars.do_empty, (m & 1) ^ 1);
@@ -163,10 +159,15 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant_
           tma_load_3d(smem + kOffDO, mdo, &bars.do_full, 0, head, q0);
           tma_load_3d(smem + kOffDO + kHalf, mdo, &bars.do_full, 64, head, q0);
         }
+        {
+          float4 w;
+          float* wp = reinterpret_cast<float*>(&w);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int r = q0 + lane * 4 + k;
-          sDelta[s * 128 + lane * 4 + k] = r < p.q_len ? delta_h[r] : 0.f;
+          for (int k = 0; k < 4; ++k) {
+            const int r = q0 + lane * 4 + k;
+            wp[k] = r < p.q_len ? delta_h[r] : 0.f;
+          }
+          *reinterpret_cast<float4*>(sDelta + s * 128 + lane * 4) = w;
         }
         mbar_arrive(&bars.do_full);
       }

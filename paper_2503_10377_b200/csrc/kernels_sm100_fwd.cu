@@ -122,6 +122,10 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
   const uint32_t tS[2] = {tmem + 0, tmem + 128};
   const uint32_t tO[2] = {tmem + 256, tmem + 384};
 
+  // register budget per warpgroup: control WG 56, softmax WGs 224 (no merge of the
+  // role branches before the teardown, so ptxas allocates per branch)
+  if (warp < 4) {
+  setmaxnreg_dec<56>();
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
@@ -167,7 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
         const uint32_t va = v_addr + stage * kTileBytes;
 #pragma unroll
         for (int k = 0; k < BN / 16; ++k)
-          mma_ts(tO[t], tS[t] + k * 8, sdesc_mnmajor(va + k * 2048, kHalf), kIdescPV, (n > 0 || k > 0) ? 1u : 0u);
+          mma_ts(tO[t], tS[t] + k * 8, sdesc_mnmajor(va + k * 2048, kHalf), kIdescPV,
+                 (n > 0 || k > 0 || !p.first) ? 1u : 0u);  // !first: O holds the carried-in state
         mma_commit(&bars.o_full[t]);
       };
       mbar_wait(&bars.q_full, 0);
@@ -199,7 +204,9 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
         mma_commit(&bars.v_empty[vs]);
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    setmaxnreg_inc<224>();
     // ===================== softmax + epilogue =====================
     const int t = (warp - 4) >> 2;                 // Q tile of this warpgroup
     const int wq = warp & 3;                       // TMEM lane quarter
@@ -238,8 +245,34 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
         mx3 = fmaxf(mx3, s[j + 3]);
       }
       const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
-      if (n == 0) {
+      if (n == 0 && p.first) {
         m_used = (mx == -INFINITY) ? 0.f : mx;
+      } else if (n == 0) {
+        // carry-in of an earlier window: natural-log m, l and the
+        // unnormalised o_acc row, rescaled to the merged max and written into O
+        const bool ok = row < p.q_len;
+        const size_t vi = (size_t)head * p.q_len + row;
+        const float m_in = ok ? p.m[vi] * kLog2e : -INFINITY;
+        const float l_in = ok ? p.l[vi] : 0.f;
+        m_used = fmaxf(m_in, mx);
+        if (m_used == -INFINITY) m_used = 0.f;
+        const float f = (m_in == -INFINITY) ? 0.f : ex2(m_in - m_used);
+        l = l_in * f;
+        const float4* src = reinterpret_cast<const float4*>(p.o_acc + ((size_t)row * p.heads + head) * HD);
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb) {
+          uint32_t o[32];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            const float4 x = ok ? src[cb * 8 + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+            o[4 * v + 0] = __float_as_uint(x.x * f);
+            o[4 * v + 1] = __float_as_uint(x.y * f);
+            o[4 * v + 2] = __float_as_uint(x.z * f);
+            o[4 * v + 3] = __float_as_uint(x.w * f);
+          }
+          tmem_st32(sO + cb * 32, o);
+        }
+        tmem_wait_st();
       } else {
         const bool need = mx > m_used + kRescaleThreshold;
         if (__any_sync(0xffffffffu, need)) {
@@ -264,18 +297,18 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       }
       const float neg_m = -m_used;
       float ls0 = 0.f, ls1 = 0.f;
-      uint32_t pk[64];
+      // P packed in place over the first 64 registers of r[] (r[j/2] <- (p_j, p_j+1))
 #pragma unroll
       for (int j = 0; j < BN; j += 2) {
         const float e0 = ex2(fmaf(s[j], sl2, neg_m));
         const float e1 = ex2(fmaf(s[j + 1], sl2, neg_m));
         ls0 += e0;
         ls1 += e1;
-        pk[j >> 1] = pack_bf16(e0, e1);
+        r[j >> 1] = pack_bf16(e0, e1);
       }
       l += ls0 + ls1;
-      tmem_st32(sS + 0, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-      tmem_st32(sS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+      tmem_st32(sS + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+      tmem_st32(sS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bars.p_full[t]);
@@ -284,10 +317,30 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       mbar_wait(&bars.o_full[t], (Tt - 1) & 1);
       tc_fence_after();
       const bool ok = row < p.q_len;
+      if (!p.last) {
+        // carry-out for the next window: unnormalised O, natural-log m, l
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb) {
+          uint32_t o[32];
+          tmem_ld32(sO + cb * 32, o);
+          tmem_wait_ld();
+          if (ok) {
+            float4* dst = reinterpret_cast<float4*>(p.o_acc + ((size_t)row * p.heads + head) * HD + cb * 32);
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+              dst[v] = make_float4(__uint_as_float(o[4 * v]), __uint_as_float(o[4 * v + 1]),
+                                   __uint_as_float(o[4 * v + 2]), __uint_as_float(o[4 * v + 3]));
+          }
+        }
+        if (ok) {
+          p.m[(size_t)head * p.q_len + row] = m_used * 0.6931471805599453f;
+          p.l[(size_t)head * p.q_len + row] = l;
+        }
+      }
       const float inv = 1.f / l;
       __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + ((size_t)row * p.heads + head) * HD;
 #pragma unroll
-      for (int cb = 0; cb < 4; ++cb) {
+      for (int cb = 0; cb < 4 && p.last; ++cb) {
         uint32_t o[32];
         tmem_ld32(sO + cb * 32, o);
         tmem_wait_ld();
@@ -304,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
           }
         }
       }
-      if (ok) p.lse[(size_t)head * p.q_len + row] = (m_used + __log2f(l)) * 0.6931471805599453f;
+      if (ok && p.last) p.lse[(size_t)head * p.q_len + row] = (m_used + __log2f(l)) * 0.6931471805599453f;
     }
   }
   tc_fence_before();
@@ -316,7 +369,6 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
 
 cudaError_t launch_fwd_sm100(const Sm100Fwd& a, cudaStream_t s) {
   if (a.p.d != HD) return cudaErrorNotSupported;
-  if (!(a.p.first && a.p.last)) return cudaErrorNotSupported;  // split windows: TODO carry state
   static bool init = false;
   if (!init) {
     cudaError_t e = cudaFuncSetAttribute(fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);

@@ -302,6 +302,8 @@ sppo_status sppo_attn_fwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
   const bool need_state = !(first && last);
   if (need_state && (!st || !st->o_acc || !st->m || !st->l))
     return fail(SPPO_E_ARG, "split windows need a carry state (o_acc, m, l)");
+  if (need_state && (!aligned16(st->o_acc) || !aligned4(st->m) || !aligned4(st->l)))
+    return fail(SPPO_E_ALIGN, "carry state: o_acc needs 16B, m/l 4B alignment");
   std::lock_guard<std::mutex> lock(ctx->mu);
   const Coverage* cov = nullptr;
   if ((s = lookup_coverage(ctx->cov_fwd, q, chunk, first, &cov))) return s;
@@ -331,8 +333,6 @@ sppo_status sppo_attn_fwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
     fill_window(L, kv, &w);
     e = launch_fwd_simt_f32(p, w, strm);
   } else {
-    if (!(first && last))
-      return fail(SPPO_E_UNSUPPORTED, "bf16 forward with split windows is not implemented yet (pass FIRST|LAST)");
     static Sm100Fwd a;
     a.p = p;
     a.n = kv->n;

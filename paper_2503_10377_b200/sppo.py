@@ -123,6 +123,9 @@ def _event(e):
         return None
     if isinstance(e, int):
         return e
+    if not e.cuda_event:  # torch creates the CUDA event lazily, on first record
+        import torch
+        e.record(torch.cuda.current_stream())
     return e.cuda_event
 
 

@@ -130,3 +130,23 @@ def test_bf16_gradient_identities(ctx):
     scale = np.abs(eng.dk.double().cpu().numpy()).sum(0).max()
     assert np.abs(dk).max() < 1e-2 * scale
     np.testing.assert_allclose(dv, xn["do"].sum(0), atol=0.3, rtol=1e-2)
+
+
+def test_bf16_forward_split_windows(ctx):
+    """Forward over windows of 2 prior chunks: (o_acc, m, l) carried between
+    launches; equals the oracle and the single-window run."""
+    off = [0, 200, 512, 700, 1024, 1300]
+    eng_w, xn = fwd_only(ctx, 1300, 2, off, seed=11, window=2)
+    eng_1, _ = fwd_only(ctx, 1300, 2, off, seed=11)
+    o, lse = oracle.causal_attention_dense(xn["q"], xn["k"], xn["v"])
+    np.testing.assert_allclose(eng_w.o.double().cpu().numpy(), o, **O_TOL)
+    np.testing.assert_allclose(eng_w.lse_heads_major().double().cpu().numpy(), lse, **LSE_TOL)
+    assert (eng_w.o.float() - eng_1.o.float()).abs().max().item() < 1.6e-2
+    # full step with windows in both directions
+    from paper_2503_10377_b200 import engine, sppo
+    x, dev = make(1300, 2, 12)
+    L = sppo.Layout(2, 128, off, dtype=sppo.SPPO_BF16)
+    eng = engine.ChunkedAttention(ctx, L, window=3)
+    eng.step(dev["q"], dev["k"], dev["v"], dev["do"])
+    torch.cuda.synchronize()
+    check_grads(eng, {k: v.double().numpy() for k, v in x.items()})
