@@ -35,6 +35,7 @@ struct FwdParams {
   float* o_acc;  // carry (unnormalised), may be null when first&&last
   float* m;
   float* l;
+  unsigned long long* trace;  // debug: per-event clock64 stamps of CTA (0, 0), or null
 };
 
 struct BwdParams {
@@ -52,7 +53,12 @@ struct BwdParams {
   int32_t final_slot;  // window slot holding chunk i when dk/dv outputs are requested, else -1
   void* dk_out;
   void* dv_out;
+  unsigned long long* trace;  // debug: per-event clock64 stamps of CTA (0, 0), or null
 };
+
+// Debug tracing (env SPPO_TRACE=<file>): slot layout trace[iter * kTraceSlots + event]
+constexpr int kTraceSlots = 16;
+constexpr int kTraceIters = 512;
 
 // ---- SIMT kernels (fp32 path; exact FP32 FMA, no tensor cores) ----------
 cudaError_t launch_fwd_simt_f32(const FwdParams& p, const KvWindow& w, cudaStream_t s);

@@ -115,6 +115,12 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant_
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
   const uint32_t tS = tmem, tdV = tmem + 128, tdP = tmem + 256, tdK = tmem + 384;
+  // debug trace of CTA (0,0): clock64 per pipeline event (SPPO_TRACE)
+  unsigned long long* tr = (p.trace && blockIdx.x == 0 && blockIdx.y == 0) ? p.trace : nullptr;
+#define TR(slot, it)                                                              \
+  do {                                                                            \
+    if (tr && (it) < kTraceIters) tr[(it) * kTraceSlots + (slot)] = clock64();   \
+  } while (0)
 
   if (warp >= 12) {
     setmaxnreg_dec<104>();
@@ -152,6 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant_
           }
           *reinterpret_cast<float4*>(sLSE + s * 128 + lane * 4) = w;  // one conflict-free STS.128
         }
+        if (lane == 0) TR(15, m);
         mbar_arrive(&bars.q_full[s]);
         mbar_wait(&bars.do_empty, (m & 1) ^ 1);
         if (lane == 0) {
@@ -183,10 +190,13 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant_
           mma_ss(d, sdesc_kmajor(A + off), sdesc_kmajor(B + off), kIdescSS, k > 0);
         }
       };
-      auto mma_tmemA = [&](uint32_t d, uint32_t tA, uint32_t B, bool acc) {  // D (+)= A[tmem] B (B MN-major)
+      // D (+)= A[tmem] B (B MN-major).  A (P or dS, bf16 pairs) of q columns 64g..64g+63
+      // sits in TMEM columns [64g, 64g+32) of its region (each WG writes its own half).
+      auto mma_tmemA = [&](uint32_t d, uint32_t tA, uint32_t B, bool acc) {
 #pragma unroll
         for (int k = 0; k < BQ / 16; ++k)
-          mma_ts(d, tA + k * 8, sdesc_mnmajor(B + k * 2048, kHalf), kIdescTS, (acc || k > 0) ? 1u : 0u);
+          mma_ts(d, tA + (k >> 2) * 64 + (k & 3) * 8, sdesc_mnmajor(B + k * 2048, kHalf), kIdescTS,
+                 (acc || k > 0) ? 1u : 0u);
       };
       auto q_stage = [&](int m) { return q_addr + (m & 1) * kTile; };
       mbar_wait(&bars.kv_full, 0);
@@ -195,23 +205,28 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant_
       mma_kmajor(tS, k_addr, q_stage(0));  // S(0) = K Q^T
       mma_commit(&bars.s_full);
       for (int m = 0; m < M; ++m) {
+        TR(0, m);
         mbar_wait(&bars.do_full, m & 1);
         if (m > 0) mbar_wait(&bars.dq_free, (m - 1) & 1);  // reducer has read dQ(m-1) out of TMEM
         tc_fence_after();
+        TR(1, m);
         mma_kmajor(tdP, v_addr, do_addr);  // dP = V dO^T
         mma_commit(&bars.dp_full);
         mbar_wait(&bars.p_full, m & 1);
         tc_fence_after();
+        TR(2, m);
         mma_tmemA(tdV, tS, do_addr, m > 0);  // dV += P^T dO
         mma_commit(&bars.do_empty);
         if (m + 1 < M) {
           mbar_wait(&bars.q_full[(m + 1) & 1], ((m + 1) >> 1) & 1);
           tc_fence_after();
+          TR(3, m);
           mma_kmajor(tS, k_addr, q_stage(m + 1));  // S(m+1): P(m) already consumed (in-order pipe)
           mma_commit(&bars.s_full);
         }
         mbar_wait(&bars.ds_full, m & 1);
         tc_fence_after();
+        TR(4, m);
         mma_tmemA(tdK, tdP, q_stage(m), m > 0);  // dK += dS^T Q
         mma_commit(&bars.q_empty[m & 1]);
 #pragma unroll
@@ -219,6 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant_
           mma_ss(tdP, sdesc_mnmajor(ds_addr + k * 2048, kHalf), sdesc_mnmajor(k_addr + k * 2048, kHalf), kIdescDQ,
                  k > 0);
         mma_commit(&bars.dq_full);
+        TR(5, m);
       }
       mma_commit(&bars.dkdv_done);
     }
@@ -226,18 +242,21 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant_
     setmaxnreg_inc<136>();
     // ===================== dQ reducer (TMEM lane = q row) =====================
     const CUtensorMap* mdq = tmap(a, a.dq_slot);
+    const float tau = p.scale;
     const int row = warp * 32 + lane;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     int piece_ctr = 0;
     for (int m = 0; m < M; ++m) {
       const int q0 = qtile(m) * BQ;
       mbar_wait(&bars.dq_full, m & 1);
+      if (threadIdx.x == 0) TR(12, m);
       tc_fence_after();
       uint32_t v[128];
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb) tmem_ld32(tdP + lane_off + cb * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[cb * 32]));
       tmem_wait_ld();
       tc_fence_before();
+      if (threadIdx.x == 0) TR(13, m);
       mbar_arrive(&bars.dq_free);
 #pragma unroll
       for (int pc = 0; pc < 4; ++pc, ++piece_ctr) {
@@ -246,13 +265,12 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant_
         if (threadIdx.x == 0) bulk_wait_read<1>();  // the reduce that last read `buf` is done
         named_bar_sync(5, 128);
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-          uint4 w;
-          w.x = v[pc * 32 + ch * 4 + 0];
-          w.y = v[pc * 32 + ch * 4 + 1];
-          w.z = v[pc * 32 + ch * 4 + 2];
-          w.w = v[pc * 32 + ch * 4 + 3];
-          *reinterpret_cast<uint4*>(stg + sw128(row, ch * 16)) = w;
+        for (int ch = 0; ch < 8; ++ch) {  // dQ = tau (dS K): tau applied here (dS is unscaled)
+          const float2 x0 = fmul2(make_float2(__uint_as_float(v[pc * 32 + ch * 4 + 0]),
+                                              __uint_as_float(v[pc * 32 + ch * 4 + 1])), make_float2(tau, tau));
+          const float2 x1 = fmul2(make_float2(__uint_as_float(v[pc * 32 + ch * 4 + 2]),
+                                              __uint_as_float(v[pc * 32 + ch * 4 + 3])), make_float2(tau, tau));
+          *reinterpret_cast<float4*>(stg + sw128(row, ch * 16)) = make_float4(x0.x, x0.y, x1.x, x1.y);
         }
         fence_proxy_async_smem();
         named_bar_sync(5, 128);
@@ -282,60 +300,81 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant_
       mbar_wait(&bars.q_full[s], (m >> 1) & 1);
       mbar_wait(&bars.do_full, m & 1);
       mbar_wait(&bars.s_full, m & 1);
+      if (lane == 0 && wq == 0) TR(6 + 4 * g, m);
       tc_fence_after();
-      float pr[64];
-      tmem_ld32(tS + lane_off + g * 64, *reinterpret_cast<uint32_t(*)[32]>(&pr[0]));
-      tmem_ld32(tS + lane_off + g * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&pr[32]));
-      tmem_wait_ld();
-      named_bar_sync(1 + wq, 64);  // partner warp finished reading S before P overwrites it
+      // ---- P = exp2(S tau log2e - LSE log2e) for q columns [64g, 64g+64); two 32-column
+      //      halves so the second TMEM load overlaps the first half's math
+      const uint32_t tSg = tS + lane_off + g * 64;
       const float* lse2 = sLSE + s * 128 + g * 64;
       // column j visible iff q position >= key position and the key row exists
       const int first_vis = kv_ok ? (kv_pos - qpos0) : 1 << 30;  // columns j >= first_vis are visible
+      const bool masked = __any_sync(0xffffffffu, first_vis > 0);
+      float2 pr[32];
+      uint32_t pk[32];
+      tmem_ld32(tSg, *reinterpret_cast<uint32_t(*)[32]>(&pr[0]));
+      tmem_wait_ld();
+      tmem_ld32(tSg + 32, *reinterpret_cast<uint32_t(*)[32]>(&pr[16]));
 #pragma unroll
-      for (int j = 0; j < 64; j += 4) {
-        const float4 l4 = *reinterpret_cast<const float4*>(lse2 + j);
-        pr[j + 0] = (j + 0 >= first_vis) ? ex2(fmaf(pr[j + 0], sl2, -l4.x)) : 0.f;
-        pr[j + 1] = (j + 1 >= first_vis) ? ex2(fmaf(pr[j + 1], sl2, -l4.y)) : 0.f;
-        pr[j + 2] = (j + 2 >= first_vis) ? ex2(fmaf(pr[j + 2], sl2, -l4.z)) : 0.f;
-        pr[j + 3] = (j + 3 >= first_vis) ? ex2(fmaf(pr[j + 3], sl2, -l4.w)) : 0.f;
-      }
-      {
-        uint32_t pk[32];
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1) tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) pk[j] = pack_bf16(pr[2 * j], pr[2 * j + 1]);
-        tmem_st32(tS + lane_off + g * 32, pk);  // P^T as bf16 pairs: A operand of dV += P^T dO
+        for (int c = 16 * h; c < 16 * h + 16; c += 2) {
+          const float4 l4 = *reinterpret_cast<const float4*>(lse2 + 2 * c);
+          float2 x0 = ffma2(pr[c], make_float2(sl2, sl2), make_float2(-l4.x, -l4.y));
+          float2 x1 = ffma2(pr[c + 1], make_float2(sl2, sl2), make_float2(-l4.z, -l4.w));
+          if (masked) {
+            const int j = 2 * c;
+            x0.x = (j + 0 >= first_vis) ? x0.x : -INFINITY;
+            x0.y = (j + 1 >= first_vis) ? x0.y : -INFINITY;
+            x1.x = (j + 2 >= first_vis) ? x1.x : -INFINITY;
+            x1.y = (j + 3 >= first_vis) ? x1.y : -INFINITY;
+          }
+          pr[c] = make_float2(ex2(x0.x), ex2(x0.y));
+          pr[c + 1] = make_float2(ex2(x1.x), ex2(x1.y));
+          pk[c] = pack_bf16(pr[c].x, pr[c].y);
+          pk[c + 1] = pack_bf16(pr[c + 1].x, pr[c + 1].y);
+        }
+        // P^T bf16 pairs into this WG's own S columns: A operand of dV += P^T dO
+        tmem_st16(tSg + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&pk[16 * h]));
       }
       tmem_wait_st();
       tc_fence_before();
+      if (lane == 0 && wq == 0 && g == 0) TR(7, m);
       mbar_arrive(&bars.p_full);
 
+      // ---- dS = P (dP - Delta)   (tau is applied to dK / dQ at their write-out)
       mbar_wait(&bars.dp_full, m & 1);
+      if (lane == 0 && wq == 0 && g == 0) TR(8, m);
       tc_fence_after();
-      float dp[64];
-      tmem_ld32(tdP + lane_off + g * 64, *reinterpret_cast<uint32_t(*)[32]>(&dp[0]));
-      tmem_ld32(tdP + lane_off + g * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&dp[32]));
-      tmem_wait_ld();
-      named_bar_sync(1 + wq, 64);  // partner finished reading dP before dS overwrites it
+      const uint32_t tPg = tdP + lane_off + g * 64;
       const float* dl = sDelta + s * 128 + g * 64;
-      uint32_t pk[32];
+      float2 dp[32];
+      tmem_ld32(tPg, *reinterpret_cast<uint32_t(*)[32]>(&dp[0]));
+      tmem_wait_ld();
+      tmem_ld32(tPg + 32, *reinterpret_cast<uint32_t(*)[32]>(&dp[16]));
 #pragma unroll
-      for (int j = 0; j < 64; j += 4) {
-        const float4 d4 = *reinterpret_cast<const float4*>(dl + j);
-        const float a0 = pr[j + 0] * tau * (dp[j + 0] - d4.x);
-        const float a1 = pr[j + 1] * tau * (dp[j + 1] - d4.y);
-        const float a2 = pr[j + 2] * tau * (dp[j + 2] - d4.z);
-        const float a3 = pr[j + 3] * tau * (dp[j + 3] - d4.w);
-        pk[j / 2] = pack_bf16(a0, a1);
-        pk[j / 2 + 1] = pack_bf16(a2, a3);
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1) tmem_wait_ld();
+#pragma unroll
+        for (int c = 16 * h; c < 16 * h + 16; c += 2) {
+          const float4 d4 = *reinterpret_cast<const float4*>(dl + 2 * c);
+          const float2 t0 = fadd2(dp[c], make_float2(-d4.x, -d4.y));
+          const float2 t1 = fadd2(dp[c + 1], make_float2(-d4.z, -d4.w));
+          const float2 a0 = fmul2(pr[c], t0);
+          const float2 a1 = fmul2(pr[c + 1], t1);
+          pk[c] = pack_bf16(a0.x, a0.y);
+          pk[c + 1] = pack_bf16(a1.x, a1.y);
+        }
+        tmem_st16(tPg + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&pk[16 * h]));  // dS^T: A of dK += dS^T Q
+#pragma unroll
+        for (int ch = 4 * h; ch < 4 * h + 4; ++ch)  // dS as MN-major A of dQ = dS K: row = key, 64 q per half
+          *reinterpret_cast<uint4*>(sDS + sw128(row, ch * 16)) =
+              make_uint4(pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
       }
-      tmem_st32(tdP + lane_off + g * 32, pk);  // dS^T bf16: A operand of dK += dS^T Q
-#pragma unroll
-      for (int ch = 0; ch < 8; ++ch)           // dS as MN-major A of dQ = dS K: row = key, 64 q per half
-        *reinterpret_cast<uint4*>(sDS + sw128(row, ch * 16)) =
-            make_uint4(pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
       tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
+      if (lane == 0 && wq == 0) TR(9 + 2 * g, m);
       mbar_arrive(&bars.ds_full);
     }
     // ---- epilogue: dK_j, dV_j of this key tile (+= into the fp32 accumulators)
@@ -359,10 +398,11 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant_
           for (int q4 = 0; q4 < 8; ++q4) {
             float4* ap = reinterpret_cast<float4*>(acc + half * 32 + q4 * 4);
             float4 o = *ap;
-            o.x += __uint_as_float(v[q4 * 4 + 0]);
-            o.y += __uint_as_float(v[q4 * 4 + 1]);
-            o.z += __uint_as_float(v[q4 * 4 + 2]);
-            o.w += __uint_as_float(v[q4 * 4 + 3]);
+            const float f = which == 0 ? 1.f : tau;  // dK = tau dS^T Q
+            o.x += __uint_as_float(v[q4 * 4 + 0]) * f;
+            o.y += __uint_as_float(v[q4 * 4 + 1]) * f;
+            o.z += __uint_as_float(v[q4 * 4 + 2]) * f;
+            o.w += __uint_as_float(v[q4 * 4 + 3]) * f;
             if (final_out) {
               uint2 b;
               b.x = pack_bf16(o.x, o.y);

@@ -103,7 +103,39 @@ struct sppo_ctx_s {
   std::unordered_map<const void*, Coverage> cov_fwd, cov_bwd;
   std::unordered_set<void*> host_allocs;
   std::mutex mu;
+  // debug tracing (env SPPO_TRACE=<file>, SPPO_TRACE_CHUNK=<i>, SPPO_TRACE_KIND=fwd|bwd):
+  // clock64 stamps of CTA (0,0) of one launch, dumped by sppo_ctx_sync
+  unsigned long long* trace = nullptr;
+  int trace_chunk = -1;
+  int trace_bwd = 1;
 };
+
+namespace {
+constexpr size_t kTraceWords = (size_t)sppo::kTraceIters * sppo::kTraceSlots;
+
+unsigned long long* trace_for(sppo_ctx ctx, int chunk, bool bwd) {
+  if (!ctx->trace) return nullptr;
+  return (chunk == ctx->trace_chunk && (int)bwd == ctx->trace_bwd) ? ctx->trace : nullptr;
+}
+
+void trace_dump(sppo_ctx ctx) {
+  const char* path = getenv("SPPO_TRACE");
+  if (!ctx->trace || !path) return;
+  std::vector<unsigned long long> h(kTraceWords);
+  if (cudaMemcpy(h.data(), ctx->trace, kTraceWords * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  FILE* f = fopen(path, "w");
+  if (!f) return;
+  for (int it = 0; it < sppo::kTraceIters; ++it) {
+    bool any = false;
+    for (int s = 0; s < sppo::kTraceSlots; ++s) any |= h[it * sppo::kTraceSlots + s] != 0;
+    if (!any) continue;
+    fprintf(f, "%d", it);
+    for (int s = 0; s < sppo::kTraceSlots; ++s) fprintf(f, " %llu", h[it * sppo::kTraceSlots + s]);
+    fprintf(f, "\n");
+  }
+  fclose(f);
+}
+}  // namespace
 
 namespace {
 
@@ -259,6 +291,15 @@ sppo_status sppo_ctx_create(int device, sppo_ctx* out) {
     sppo_ctx_destroy(c);
     return cuda_fail(e, "sppo_ctx_create");
   }
+  if (getenv("SPPO_TRACE")) {
+    const char* ch = getenv("SPPO_TRACE_CHUNK");
+    const char* kind = getenv("SPPO_TRACE_KIND");
+    c->trace_chunk = ch ? atoi(ch) : 0;
+    c->trace_bwd = (kind && strcmp(kind, "fwd") == 0) ? 0 : 1;
+    if (cudaMalloc(&c->trace, kTraceWords * 8) != cudaSuccess ||
+        cudaMemset(c->trace, 0, kTraceWords * 8) != cudaSuccess)
+      c->trace = nullptr;
+  }
   *out = c;
   return SPPO_OK;
 }
@@ -275,6 +316,7 @@ sppo_status sppo_ctx_destroy(sppo_ctx c) {
   if (c->ev_copy) cudaEventDestroy(c->ev_copy);
   if (c->desc_dev) cudaFree(c->desc_dev);
   if (c->desc_host) cudaFreeHost(c->desc_host);
+  if (c->trace) cudaFree(c->trace);
   delete c;
   return SPPO_OK;
 }
@@ -284,6 +326,7 @@ sppo_status sppo_ctx_sync(sppo_ctx c) {
   SPPO_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
   SPPO_CUDA(cudaDeviceSynchronize(), "device fault");
   SPPO_CUDA(cudaGetLastError(), "device fault");
+  trace_dump(c);
   return SPPO_OK;
 }
 
@@ -322,6 +365,7 @@ sppo_status sppo_attn_fwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
   p.q = q;
   p.o = o;
   p.lse = lse;
+  p.trace = trace_for(ctx, chunk, false);
   if (st) {
     p.o_acc = st->o_acc;
     p.m = st->m;
@@ -413,6 +457,7 @@ sppo_status sppo_attn_bwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
   p.final_slot = a->dk ? final_slot : -1;
   p.dk_out = a->dk;
   p.dv_out = a->dv;
+  p.trace = trace_for(ctx, chunk, true);
   const bool bf16 = L->dtype == SPPO_BF16;
   cudaError_t e = cudaSuccess;
   if (first) e = launch_bwd_preprocess(p, bf16, strm);  // Delta_i, dq_acc = 0  (a5)

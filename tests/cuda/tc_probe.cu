@@ -132,6 +132,53 @@ __global__ void __launch_bounds__(128, 1) probe_kernel(int mode, const __nv_bflo
   if (warp == 0) tmem_dealloc<256>(tbase);
 }
 
+// MMA throughput microbenchmark: thread 0 issues `reps` x 8 MMAs (128 x N x 16
+// each, K = 128 per group) of one operand mode back to back, commit, wait; the
+// clock64 delta per 128x N x 128 group is written to out[0].  Operands are
+// uninitialised smem (values irrelevant for timing).
+template <int N>
+__global__ void __launch_bounds__(128, 1) mma_bench_kernel(int mode, int reps, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tmem_base;
+  if (threadIdx.x == 0) {
+    const uint32_t sA = smem_u32(smem), sB = smem_u32(smem + 32768);
+    const uint32_t a_mn = (mode == 3) ? 1 : 0, b_mn = (mode == 0) ? 0 : 1;
+    const uint32_t idesc = idesc_bf16(128, N, a_mn, b_mn);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint64_t bd = b_mn ? sdesc_mnmajor(sB + k * 2048, 16384) : sdesc_kmajor(sB + (k / 4) * 16384 + (k % 4) * 32);
+        if (mode == 2) {
+          mma_ts(tb, tb + 128 + k * 8, bd, idesc, 1);
+        } else {
+          const uint64_t ad = a_mn ? sdesc_mnmajor(sA + k * 2048, 16384) : sdesc_kmajor(sA + (k / 4) * 16384 + (k % 4) * 32);
+          mma_ss(tb, ad, bd, idesc, 1);
+        }
+      }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    out[0] = (t1 - t0) / reps;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<256>(tb);
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -152,6 +199,23 @@ int encode(CUtensorMap* m, const void* p, int rows, int cols, int box_rows) {
 }
 
 }  // namespace
+
+extern "C" long long tc_mma_bench(int mode, int N, int reps) {
+  long long* d = nullptr;
+  long long h = -1;
+  if (cudaMalloc(&d, sizeof(long long)) != cudaSuccess) return -1;
+  const int smem = 65536 + 1024;
+  if (N == 128) {
+    cudaFuncSetAttribute(mma_bench_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    mma_bench_kernel<128><<<1, 128, smem>>>(mode, reps, d);
+  } else {
+    cudaFuncSetAttribute(mma_bench_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    mma_bench_kernel<64><<<1, 128, smem>>>(mode, reps, d);
+  }
+  if (cudaDeviceSynchronize() == cudaSuccess) cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return h;
+}
 
 extern "C" int tc_probe_run(int mode, int N, int use_tma, const void* A, const void* B, float* D) {
   CUtensorMap* maps = nullptr;
