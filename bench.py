@@ -137,19 +137,13 @@ def dist_setup():
 
 
 def head_range(heads, ws, rank):
-    if heads % ws:
-        raise SystemExit(f"heads={heads} not divisible by {ws} GPUs")
-    per = heads // ws
-    return list(range(rank * per, (rank + 1) * per))
+    from paper_2503_10377_b200.dist import head_range as hr
+    return hr(heads, ws, rank)
 
 
 def max_over_ranks(x, ws):
-    if ws == 1:
-        return x
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2503_10377_b200.dist import max_over_ranks as mx
+    return mx(x, ws, device="cuda" if torch.cuda.is_available() else "cpu")
 
 
 def barrier(ws):
@@ -272,16 +266,39 @@ def run_ours(args, cfg, ws, rank, local):
                    "alpha": [round(a, 3) for a in alpha], "bw_d2h_gbs_assumed": bw / 1e9}
         eng.free_host()
 
+    # ---- KV streaming policy (hot prefix resident, colder chunks streamed from host)
+    kvs = None
+    if args.kv_hot >= 0:
+        res = []
+        st = None
+        for rep in range(1 + max(1, args.steps // 2)):
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            st = eng.step_kv_stream(x["q"], x["k"], x["v"], x["do"], hot=args.kv_hot, window=args.kv_window,
+                                    stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if rep > 0:
+                res.append(e0.elapsed_time(e1))
+        kv_ms = max_over_ranks(statistics.median(res), ws)
+        kvs = {"policy": f"kv hot-prefix P={args.kv_hot} resident, chunks >= P streamed H2D in windows of "
+                         f"{args.kv_window} (2-slot ring) for every later fwd/bwd; Type-1 resident",
+               "ms_per_step": round(kv_ms, 3), "resident_ms_per_step": round(ms, 3),
+               "exposed_pct": round(100.0 * (kv_ms - ms) / ms, 2), "h2d_bytes": st["h2d"], "d2h_bytes": st["d2h"],
+               "h2d_gbs_achieved": round(st["h2d"] / (kv_ms * 1e-3) / 1e9, 1), "windows": st["windows"]}
+        eng.free_host()
+
     # ---- final gather of O over NCCL (multi-GPU only, not timed in value)
     gather = None
     if ws > 1:
-        import torch.distributed as dist
-        out = torch.empty((ws,) + tuple(eng.o.shape), dtype=eng.o.dtype, device=dev)
+        from paper_2503_10377_b200.dist import gather_heads
         g0 = time.perf_counter()
-        dist.all_gather_into_tensor(out, eng.o.contiguous())
+        full = gather_heads(eng.o, ws)
         torch.cuda.synchronize()
         gather = {"op": "all_gather_into_tensor(O) over NCCL", "ms": round((time.perf_counter() - g0) * 1e3, 2),
-                  "bytes": out.numel() * out.element_size()}
+                  "bytes": full.numel() * full.element_size()}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -311,7 +328,8 @@ def run_ours(args, cfg, ws, rank, local):
                      "frac": round(ach_bwd / peaks["sustained"], 3), "traffic": None,
                      "peak_kind": "sustained bf16 (kernel timed inside a long step), " + peaks["source"],
                      "share_of_step": round(bwd_ms / ms, 3)},
-        "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "offload": offload, "gather": gather,
+        "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "offload": offload, "kv_stream": kvs,
+        "gather": gather,
         "cpu_baseline": cpu,
     }
     return line
@@ -348,6 +366,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-offload", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--kv-hot", type=int, default=-1, help="also time KV streaming with this hot prefix (-1: skip)")
+    ap.add_argument("--kv-window", type=int, default=4)
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: warmup < 3 violates the timing rules", file=sys.stderr)

@@ -189,7 +189,7 @@ class ChunkedAttention:
             if poison:
                 for _, t, _, n, ev in parts:
                     strm.wait_event(ev)
-                    t.view(torch.uint8)[:n].fill_(0xFF)  # NaN pattern in bf16/fp32
+                    t.reshape(-1).view(torch.uint8)[:n].fill_(0xFF)  # first n BYTES: NaN pattern in bf16/fp32
         issued = set()
 
         def prefetch(i):
@@ -214,6 +214,132 @@ class ChunkedAttention:
                 strm.wait_event(pe)
             self.backward_chunk(i, q, k, v, do, strm)
         return moved
+
+    # one step with KV streaming (hot prefix resident, cold chunks on host) -----
+    def step_kv_stream(self, q, k, v, do, hot: int, window: int, stream=None, poison: bool = False):
+        """Forward + backward with the KV residency policy of SURVEY §8(c):
+        K_j, V_j of the hot prefix j < ``hot`` stay on the GPU (the most-accessed
+        Type-0 tensors); every colder chunk is written back to pinned host
+        memory after its forward (D2H overlapping fwd(j+1)) and streamed
+        back in windows of ``window`` chunks through a 2-slot device ring for
+        every later fwd(i) / bwd(i) (prefetch of window n+1 overlaps compute of
+        window n).  Windows of one chunk are chained with FIRST/LAST (the online
+        softmax carry, a2).  With ``poison`` the full-sequence device K/V of cold
+        chunks are overwritten with NaN once offloaded, proving that only the
+        streamed copies are read.  Returns copy statistics."""
+        L = self.L
+        N = L.num_chunks
+        h, d = L.heads, L.head_dim
+        strm = stream or torch.cuda.current_stream()
+        smax = max(L.chunk_len(i) for i in range(N))
+        key = ("ring", window, smax)
+        if getattr(self, "_ring_key", None) != key:
+            self._ring = torch.empty((2, window, 2, smax, h, d), dtype=self.o.dtype, device=self.device)
+            self._ring_key = key
+        ring = self._ring
+        stats = {"d2h": 0, "h2d": 0, "windows": 0}
+        off_done = {}
+
+        def host_of(j):
+            nb = L.chunk_len(j) * h * d * self.elem
+            return self._host_buf(("k", j), nb), self._host_buf(("v", j), nb), nb
+
+        # flat schedule of (kind, chunk, windows); a window is a list of (j, where)
+        def windows_for(i, kind):
+            hot_ids = [j for j in range(min(hot, i + 1))]
+            if kind == "fwd":
+                cold = [j for j in range(hot, i - 1)]           # i-1 and i still on device (P:369)
+                dev_ids = hot_ids + [j for j in (i - 1, i) if j >= hot and j >= 0]
+            else:
+                cold = [j for j in range(hot, i + 1)]
+                dev_ids = hot_ids
+            wins = [[(j, "dev") for j in dev_ids]] if dev_ids else []
+            wins += [[(j, "ring") for j in cold[a:a + window]] for a in range(0, len(cold), window)]
+            return wins
+
+        sched = [("fwd", i, windows_for(i, "fwd")) for i in range(N)] + \
+                [("bwd", i, windows_for(i, "bwd")) for i in range(N - 1, -1, -1)]
+        ring_windows = [(si, wi) for si, (_, _, ws) in enumerate(sched) for wi, w in enumerate(ws) if w[0][1] == "ring"]
+        ring_slot = {rw: n % 2 for n, rw in enumerate(ring_windows)}
+        ready = {}
+
+        offloaded = set(range(min(hot, N)))  # chunks whose host copy has been issued (hot ones never stream)
+
+        def prefetch(n, must=False):
+            if n >= len(ring_windows) or n in ready:
+                return
+            si, wi = ring_windows[n]
+            if not all(j in offloaded for j, _ in sched[si][2][wi]):
+                assert not must, "window streamed before its chunks were written back"
+                return  # a chunk of this window has not been offloaded yet: issue later
+            slot = n % 2
+            evs = []
+            for c, (j, _) in enumerate(sched[si][2][wi]):
+                if j in off_done:
+                    strm.wait_event(off_done.pop(j))  # its D2H must have landed before reading the host copy
+                hk, hv, nb = host_of(j)
+                for which, hp in ((0, hk), (1, hv)):
+                    dst = ring[slot, c, which, :L.chunk_len(j)]
+                    ev = torch.cuda.Event()
+                    # ordered after the compute work enqueued so far (the ring slot's last reader)
+                    self.ctx.kv_prefetch(j, hp, dst, nb, consumer=strm, done=ev, flags=sppo.SPPO_COPY_DEFER_WAIT)
+                    stats["h2d"] += nb
+                    evs.append(ev)
+            ready[n] = evs
+
+        self.dk_acc.zero_()
+        self.dv_acc.zero_()
+        n_ring = 0
+        prefetch(0)
+        for si, (kind, i, wins) in enumerate(sched):
+            s = L.chunk_len(i)
+            for wi, w in enumerate(wins):
+                flags = (sppo.SPPO_FIRST if wi == 0 else 0) | (sppo.SPPO_LAST if wi == len(wins) - 1 else 0)
+                ids = [j for j, _ in w]
+                if w[0][1] == "ring":
+                    prefetch(n_ring, must=True)  # no-op when already issued one window ahead
+                    prefetch(n_ring + 1)  # next window's copy overlaps this window's compute
+                    for ev in ready.pop(n_ring):
+                        strm.wait_event(ev)
+                    slot = n_ring % 2
+                    ks = [ring[slot, c, 0, :L.chunk_len(j)] for c, j in enumerate(ids)]
+                    vs = [ring[slot, c, 1, :L.chunk_len(j)] for c, j in enumerate(ids)]
+                    n_ring += 1
+                else:
+                    ks = [self.rows(k, j) for j in ids]
+                    vs = [self.rows(v, j) for j in ids]
+                stats["windows"] += 1
+                if kind == "fwd":
+                    self.ctx.attn_fwd(L, i, self.rows(q, i), ids, ks, vs, flags=flags,
+                                      state=None if len(wins) == 1 else (self.o_acc[:s], self.m[:s * h], self.l[:s * h]),
+                                      o=self.rows(self.o, i), lse=self.lse_view(i), stream=strm)
+                    self.launches += 1
+                else:
+                    has_i = i in ids
+                    self.ctx.attn_bwd(L, i, self.rows(q, i), ids, ks, vs, self.rows(self.o, i), self.lse_view(i),
+                                      self.rows(do, i), self.delta[:s * h], self.dq_acc[:s],
+                                      [self.rows(self.dk_acc, j) for j in ids],
+                                      [self.rows(self.dv_acc, j) for j in ids],
+                                      dq=self.rows(self.dq, i), dk=self.rows(self.dk, i) if has_i else None,
+                                      dv=self.rows(self.dv, i) if has_i else None, flags=flags, stream=strm)
+                    self.launches += 1 + (flags & sppo.SPPO_FIRST != 0) + (flags & sppo.SPPO_LAST != 0)
+            if kind == "fwd" and i >= hot:
+                # write K_i, V_i back to the host arena (Type-0 demoted by the policy); overlaps fwd(i+1)
+                hk, hv, nb = host_of(i)
+                ev = torch.cuda.Event()
+                stats["d2h"] += self.ctx.kv_offload(i, self.rows(k, i), hk, nb, 1.0, producer=strm)
+                stats["d2h"] += self.ctx.kv_offload(i, self.rows(v, i), hv, nb, 1.0, producer=strm, done=ev)
+                off_done[i] = ev
+                offloaded.add(i)
+                poison_ev = ev
+            if poison and kind == "fwd" and i - 1 >= hot:
+                # chunk i-1 has left the GPU for good (fwd(i+1) streams it): poison its device copy
+                strm.wait_event(self._last_off_ev)
+                self.rows(k, i - 1).view(torch.uint8).fill_(0xFF)
+                self.rows(v, i - 1).view(torch.uint8).fill_(0xFF)
+            if kind == "fwd" and i >= hot:
+                self._last_off_ev = poison_ev
+        return stats
 
     # end-to-end step through host buffers --------------------------------------
     def step_host_io(self, host_in, host_out, dev_in, stream=None):

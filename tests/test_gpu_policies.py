@@ -1,0 +1,87 @@
+"""GPU tests of the two-level activation manager (reading
+L8-L10): Type-1 alpha offload and KV streaming with a hot prefix, each with the
+device copies poisoned (NaN) after they leave the GPU, so the backward can only
+have read the bytes that came back over sppo_kv_prefetch."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import make_inputs
+
+pytestmark = pytest.mark.gpu
+
+O_TOL = dict(atol=2e-2, rtol=1e-2)
+G_TOL = dict(atol=5e-2, rtol=5e-2)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2503_10377_b200 import sppo
+    c = sppo.Context(0)
+    yield c
+    c.close()
+
+
+def setup(ctx, S, h, N, seed):
+    from paper_2503_10377_b200 import engine, sppo
+    x = make_inputs(S, range(h), 128, seed=seed, dtype=torch.bfloat16)
+    dev = {k: v.cuda() for k, v in x.items()}
+    L = sppo.Layout(h, 128, sppo.partition_equal(S, N))
+    return x, dev, engine.ChunkedAttention(ctx, L)
+
+
+def snapshot(eng):
+    return {k: getattr(eng, k).clone() for k in ("o", "dq", "dk", "dv")} | {"lse": eng.lse.clone()}
+
+
+def test_type1_offload_roundtrip_bitwise(ctx):
+    """alpha in (0,1] prefixes of Q, O, LSE leave the GPU after fwd(i), are
+    poisoned, and come back before bwd(i): O/LSE/dK/dV bitwise equal to the
+    resident step (same kernels, same windows); dQ (reduce-add order) within 1 ulp-ish."""
+    x, dev, eng = setup(ctx, 3072, 2, 6, seed=21)
+    eng.step(dev["q"], dev["k"], dev["v"], dev["do"])
+    torch.cuda.synchronize()
+    ref = snapshot(eng)
+    alpha = [0.3, 0.75, 1.0, 0.5, 1.0, 0.0]
+    q = dev["q"].clone()
+    moved = eng.step_offload(q, dev["k"], dev["v"], dev["do"], alpha, poison=True)
+    torch.cuda.synchronize()
+    ctx.sync()
+    assert moved["d2h"] == moved["h2d"] > 0
+    for key in ("o", "lse", "dk", "dv"):
+        got = getattr(eng, key)
+        bad = (got != ref[key]).nonzero()
+        assert bad.numel() == 0, (key, bad.shape, bad[:5].tolist(), (got.float() - ref[key].float()).abs().max().item())
+    assert (eng.dq.float() - ref["dq"].float()).abs().max().item() < 1e-2
+    eng.free_host()
+
+
+@pytest.mark.parametrize("hot,window", [(0, 2), (2, 3), (1, 1)])
+def test_kv_stream_matches_oracle(ctx, hot, window):
+    S, h, N = 2048, 2, 8
+    x, dev, eng = setup(ctx, S, h, N, seed=22 + hot)
+    k, v = dev["k"].clone(), dev["v"].clone()
+    stats = eng.step_kv_stream(dev["q"], k, v, dev["do"], hot=hot, window=window, poison=True)
+    torch.cuda.synchronize()
+    ctx.sync()
+    assert stats["h2d"] > 0
+    xn = {kk: vv.double().numpy() for kk, vv in x.items()}
+    ref = oracle.causal_attention_dense_bwd(xn["q"], xn["k"], xn["v"], xn["do"])
+    np.testing.assert_allclose(eng.o.double().cpu().numpy(), ref["o"], **O_TOL)
+    for key in ("dq", "dk", "dv"):
+        np.testing.assert_allclose(getattr(eng, key).double().cpu().numpy(), ref[key], **G_TOL, err_msg=key)
+    # the device K/V of cold chunks really were poisoned
+    assert torch.isnan(k[eng.L.offsets[max(hot, 0)]:eng.L.offsets[N - 2]].float()).all() or hot >= N - 2
+    eng.free_host()
+
+
+def test_alpha_planner_in_engine_matches_oracle(ctx):
+    """The bench's alpha: per-chunk M_i = BW * T_fwd(i+1) from measured forward
+    times; the product's sppo_offload_alpha and the oracle agree."""
+    from paper_2503_10377_b200 import sppo
+    x, dev, eng = setup(ctx, 4096, 2, 4, seed=23)
+    A = [eng.type1_bytes(i) for i in range(4)]
+    thr = [1e6, 5e6, 2e7, 0.0]
+    assert sppo.offload_alpha(A, thr, 0.0) == oracle.offload_alpha(A, thr, 0.0)
