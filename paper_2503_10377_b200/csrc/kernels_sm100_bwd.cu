@@ -48,6 +48,10 @@ constexpr uint32_t kIdescSS = idesc_bf16(128, 128, 0, 0);   // K-major x K-major
 constexpr uint32_t kIdescTS = idesc_bf16(128, 128, 0, 1);   // TMEM A x MN-major B
 constexpr uint32_t kIdescDQ = idesc_bf16(128, 128, 1, 1);   // MN-major A x MN-major B
 constexpr float kLog2e = 1.4426950408889634f;
+#ifndef SPPO_DQ_DIRECT_RED
+#define SPPO_DQ_DIRECT_RED 0  // measured: direct REDG doubles the tile period (L2/LSU bound)
+#endif
+constexpr bool kDqDirectRed = SPPO_DQ_DIRECT_RED;  // dQ: red.global from registers (1) or TMA reduce (0)
 
 struct Bars {
   uint64_t kv_full;
@@ -178,65 +182,70 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant_
         }
         mbar_arrive(&bars.do_full);
       }
-    } else if (warp == 12 && lane == 0) {
-      // ===================== MMA issuer =====================
-      const uint32_t k_addr = smem_u32(smem + kOffK), v_addr = smem_u32(smem + kOffV);
-      const uint32_t q_addr = smem_u32(smem + kOffQ), do_addr = smem_u32(smem + kOffDO);
-      const uint32_t ds_addr = smem_u32(smem + kOffDS);
-      auto mma_kmajor = [&](uint32_t d, uint32_t A, uint32_t B) {  // D = A B^T, both [128][128] K-major
+    } else if (warp == 12) {
+      // ===================== MMA issuer (whole warp, converged; one elected lane issues) =====================
+      // Base descriptors computed once; a k-step only adds (byte offset >> 4) to the
+      // 14-bit start-address field (smem < 256 KB, so no carry leaves the field).
+      const uint64_t dK_k = sdesc_kmajor(smem_u32(smem + kOffK)), dV_k = sdesc_kmajor(smem_u32(smem + kOffV));
+      const uint64_t dDO_k = sdesc_kmajor(smem_u32(smem + kOffDO));
+      const uint64_t dDO_mn = sdesc_mnmajor(smem_u32(smem + kOffDO), kHalf);
+      const uint64_t dDS_mn = sdesc_mnmajor(smem_u32(smem + kOffDS), kHalf);
+      const uint64_t dK_mn = sdesc_mnmajor(smem_u32(smem + kOffK), kHalf);
+      const uint64_t dQ_k0 = sdesc_kmajor(smem_u32(smem + kOffQ));
+      const uint64_t dQ_mn0 = sdesc_mnmajor(smem_u32(smem + kOffQ), kHalf);
+      constexpr uint64_t kStageStep = kTile >> 4;
+      auto koff = [](int k) { return (uint64_t)(((k >> 2) * kHalf + (k & 3) * 32) >> 4); };  // K-major k-step
+      auto moff = [](int k) { return (uint64_t)((k * 2048) >> 4); };                         // MN-major k-step
+      auto mma_kmajor = [&](uint32_t d, uint64_t A, uint64_t B) {  // D = A B^T, both [128][128] K-major
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k) {
-          const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
-          mma_ss(d, sdesc_kmajor(A + off), sdesc_kmajor(B + off), kIdescSS, k > 0);
-        }
+        for (int k = 0; k < HD / 16; ++k) mma_ss_w(d, A + koff(k), B + koff(k), kIdescSS, k > 0);
       };
       // D (+)= A[tmem] B (B MN-major).  A (P or dS, bf16 pairs) of q columns 64g..64g+63
       // sits in TMEM columns [64g, 64g+32) of its region (each WG writes its own half).
-      auto mma_tmemA = [&](uint32_t d, uint32_t tA, uint32_t B, bool acc) {
+      auto mma_tmemA = [&](uint32_t d, uint32_t tA, uint64_t B, bool acc) {
 #pragma unroll
         for (int k = 0; k < BQ / 16; ++k)
-          mma_ts(d, tA + (k >> 2) * 64 + (k & 3) * 8, sdesc_mnmajor(B + k * 2048, kHalf), kIdescTS,
-                 (acc || k > 0) ? 1u : 0u);
+          mma_ts_w(d, tA + (k >> 2) * 64 + (k & 3) * 8, B + moff(k), kIdescTS, (acc || k > 0) ? 1u : 0u);
       };
-      auto q_stage = [&](int m) { return q_addr + (m & 1) * kTile; };
+      auto q_k = [&](int m) { return dQ_k0 + (m & 1) * kStageStep; };
+      auto q_mn = [&](int m) { return dQ_mn0 + (m & 1) * kStageStep; };
       mbar_wait(&bars.kv_full, 0);
       mbar_wait(&bars.q_full[0], 0);
       tc_fence_after();
-      mma_kmajor(tS, k_addr, q_stage(0));  // S(0) = K Q^T
-      mma_commit(&bars.s_full);
+      mma_kmajor(tS, dK_k, q_k(0));  // S(0) = K Q^T
+      mma_commit_w(&bars.s_full);
       for (int m = 0; m < M; ++m) {
         TR(0, m);
         mbar_wait(&bars.do_full, m & 1);
         if (m > 0) mbar_wait(&bars.dq_free, (m - 1) & 1);  // reducer has read dQ(m-1) out of TMEM
         tc_fence_after();
         TR(1, m);
-        mma_kmajor(tdP, v_addr, do_addr);  // dP = V dO^T
-        mma_commit(&bars.dp_full);
+        mma_kmajor(tdP, dV_k, dDO_k);  // dP = V dO^T
+        mma_commit_w(&bars.dp_full);
         mbar_wait(&bars.p_full, m & 1);
         tc_fence_after();
         TR(2, m);
-        mma_tmemA(tdV, tS, do_addr, m > 0);  // dV += P^T dO
-        mma_commit(&bars.do_empty);
+        mma_tmemA(tdV, tS, dDO_mn, m > 0);  // dV += P^T dO
+        mma_commit_w(&bars.do_empty);
         if (m + 1 < M) {
           mbar_wait(&bars.q_full[(m + 1) & 1], ((m + 1) >> 1) & 1);
           tc_fence_after();
           TR(3, m);
-          mma_kmajor(tS, k_addr, q_stage(m + 1));  // S(m+1): P(m) already consumed (in-order pipe)
-          mma_commit(&bars.s_full);
+          mma_kmajor(tS, dK_k, q_k(m + 1));  // S(m+1): P(m) already consumed (in-order pipe)
+          mma_commit_w(&bars.s_full);
         }
         mbar_wait(&bars.ds_full, m & 1);
         tc_fence_after();
         TR(4, m);
-        mma_tmemA(tdK, tdP, q_stage(m), m > 0);  // dK += dS^T Q
-        mma_commit(&bars.q_empty[m & 1]);
+        mma_tmemA(tdK, tdP, q_mn(m), m > 0);  // dK += dS^T Q
+        mma_commit_w(&bars.q_empty[m & 1]);
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)  // dQ = dS K  (A = dS MN-major in smem, B = K MN-major)
-          mma_ss(tdP, sdesc_mnmajor(ds_addr + k * 2048, kHalf), sdesc_mnmajor(k_addr + k * 2048, kHalf), kIdescDQ,
-                 k > 0);
-        mma_commit(&bars.dq_full);
+          mma_ss_w(tdP, dDS_mn + moff(k), dK_mn + moff(k), kIdescDQ, k > 0);
+        mma_commit_w(&bars.dq_full);
         TR(5, m);
       }
-      mma_commit(&bars.dkdv_done);
+      mma_commit_w(&bars.dkdv_done);
     }
   } else if (warp < 4) {
     setmaxnreg_inc<136>();
@@ -258,6 +267,20 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_kernel(const __grid_constant_
       tc_fence_before();
       if (threadIdx.x == 0) TR(13, m);
       mbar_arrive(&bars.dq_free);
+      if constexpr (kDqDirectRed) {
+        // fp32 vector reductions straight from registers: keeps the 128 KB / tile of
+        // staging traffic off shared memory (the bwd is smem-bandwidth bound)
+        if (q0 + row < p.q_len) {
+          float* dst = p.dq_acc + ((size_t)(q0 + row) * p.heads + head) * HD;
+#pragma unroll
+          for (int c4 = 0; c4 < 32; ++c4)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * c4),
+                         "f"(__uint_as_float(v[4 * c4 + 0]) * tau), "f"(__uint_as_float(v[4 * c4 + 1]) * tau),
+                         "f"(__uint_as_float(v[4 * c4 + 2]) * tau), "f"(__uint_as_float(v[4 * c4 + 3]) * tau)
+                         : "memory");
+        }
+        continue;
+      }
 #pragma unroll
       for (int pc = 0; pc < 4; ++pc, ++piece_ctr) {
         const int buf = piece_ctr & 1;

@@ -121,6 +121,11 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
   const uint32_t tmem = bars.tmem_base;
   const uint32_t tS[2] = {tmem + 0, tmem + 128};
   const uint32_t tO[2] = {tmem + 256, tmem + 384};
+  unsigned long long* tr = (p.trace && blockIdx.x == 0 && blockIdx.y == 0) ? p.trace : nullptr;
+#define TR(slot, it)                                                            \
+  do {                                                                          \
+    if (tr && (it) < kTraceIters) tr[(it) * kTraceSlots + (slot)] = clock64(); \
+  } while (0)
 
   // register budget per warpgroup: control WG 56, softmax WGs 224 (no merge of the
   // role branches before the teardown, so ptxas allocates per branch)
@@ -145,10 +150,12 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
         const CUtensorMap* mv = tmap(a, a.slots.v[cur.c]);
         const int row = cur.tt * BN;
         mbar_wait(&bars.k_empty[s], ph ^ 1);
+        TR(11, n);
         mbar_arrive_expect_tx(&bars.k_full[s], kTileBytes);
         tma_load_3d(sK + s * kTileBytes, mk, &bars.k_full[s], 0, head, row);
         tma_load_3d(sK + s * kTileBytes + kHalf, mk, &bars.k_full[s], 64, head, row);
         mbar_wait(&bars.v_empty[s], ph ^ 1);
+        TR(12, n);
         mbar_arrive_expect_tx(&bars.v_full[s], kTileBytes);
         tma_load_3d(sV + s * kTileBytes, mv, &bars.v_full[s], 0, head, row);
         tma_load_3d(sV + s * kTileBytes + kHalf, mv, &bars.v_full[s], 64, head, row);
@@ -156,52 +163,58 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    if (lane == 0 && Tn > 0) {
-      const uint32_t q_addr = smem_u32(sQ), k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+    if (Tn > 0) {  // whole warp, converged; one elected lane issues (mma_*_w)
+      // base descriptors once; a k-step adds (byte offset >> 4) to the start-address field
+      const uint64_t dQ0 = sdesc_kmajor(smem_u32(sQ)), dK0 = sdesc_kmajor(smem_u32(sK));
+      const uint64_t dV0 = sdesc_mnmajor(smem_u32(sV), kHalf);
+      constexpr uint64_t kStep = kTileBytes >> 4;
       auto issue_s = [&](int t, int stage) {
-        const uint32_t qa = q_addr + t * kTileBytes, ka = k_addr + stage * kTileBytes;
+        const uint64_t qa = dQ0 + t * kStep, ka = dK0 + stage * kStep;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
-          const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
-          mma_ss(tS[t], sdesc_kmajor(qa + off), sdesc_kmajor(ka + off), kIdescS, k > 0);
+          const uint64_t off = ((k >> 2) * kHalf + (k & 3) * 32) >> 4;
+          mma_ss_w(tS[t], qa + off, ka + off, kIdescS, k > 0);
         }
-        mma_commit(&bars.s_full[t]);
+        mma_commit_w(&bars.s_full[t]);
       };
       auto issue_pv = [&](int t, int stage, int n) {
-        const uint32_t va = v_addr + stage * kTileBytes;
+        const uint64_t va = dV0 + stage * kStep;
 #pragma unroll
         for (int k = 0; k < BN / 16; ++k)
-          mma_ts(tO[t], tS[t] + k * 8, sdesc_mnmajor(va + k * 2048, kHalf), kIdescPV,
-                 (n > 0 || k > 0 || !p.first) ? 1u : 0u);  // !first: O holds the carried-in state
-        mma_commit(&bars.o_full[t]);
+          mma_ts_w(tO[t], tS[t] + k * 8, va + ((k * 2048) >> 4), kIdescPV,
+                   (n > 0 || k > 0 || !p.first) ? 1u : 0u);  // !first: O holds the carried-in state
+        mma_commit_w(&bars.o_full[t]);
       };
       mbar_wait(&bars.q_full, 0);
       mbar_wait(&bars.k_full[0], 0);
       tc_fence_after();
       if (T[0] > 0) issue_s(0, 0);
       if (T[1] > 0) issue_s(1, 0);
-      mma_commit(&bars.k_empty[0]);
+      mma_commit_w(&bars.k_empty[0]);
       for (int n = 0; n < Tn; ++n) {
         const int vs = n & 1;
         const int nx = n + 1, ks = nx & 1;
         const uint32_t kph = (nx >> 1) & 1;
         mbar_wait(&bars.v_full[vs], (n >> 1) & 1);
+        TR(0, n);
         tc_fence_after();
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
           if (n < T[t]) {
             mbar_wait(&bars.p_full[t], n & 1);
             tc_fence_after();
+            TR(1 + 2 * t, n);
             issue_pv(t, vs, n);
             if (nx < T[t]) {
               mbar_wait(&bars.k_full[ks], kph);
               tc_fence_after();
+              TR(2 + 2 * t, n);
               issue_s(t, ks);
             }
           }
         }
-        if (nx < Tn) mma_commit(&bars.k_empty[ks]);
-        mma_commit(&bars.v_empty[vs]);
+        if (nx < Tn) mma_commit_w(&bars.k_empty[ks]);
+        mma_commit_w(&bars.v_empty[vs]);
       }
     }
   }
@@ -224,6 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       const int valid = min(BN, a.len[cur.c] - cur.tt * BN);
       const int limit = min(valid, pos - kpos0 + 1);  // columns >= limit are masked
       mbar_wait(&bars.s_full[t], n & 1);
+      if (lane == 0 && wq == 0) TR(5 + 3 * t, n);
       tc_fence_after();
       uint32_t r[128];
       tmem_ld32(sS + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
@@ -295,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
           tmem_wait_st();
         }
       }
+      if (lane == 0 && wq == 0) TR(6 + 3 * t, n);
       const float neg_m = -m_used;
       float ls0 = 0.f, ls1 = 0.f;
       // P packed in place over the first 64 registers of r[] (r[j/2] <- (p_j, p_j+1))
@@ -311,6 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       tmem_st32(sS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
       tmem_wait_st();
       tc_fence_before();
+      if (lane == 0 && wq == 0) TR(7 + 3 * t, n);
       mbar_arrive(&bars.p_full[t]);
     }
     if (Tt > 0) {
