@@ -36,6 +36,7 @@ constexpr uint32_t kHalf = kTileBytes / 2;       // one box: 128 rows x 64 cols
 constexpr int kSmemBytes = 6 * kTileBytes + 1024;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;        // log2 units
+constexpr int kEmuEvery = 8;                     // 1 of every kEmuEvery exp2 pairs on the FMA pipe
 
 constexpr uint32_t kIdescS = idesc_bf16(128, 128, 0, 0);   // Q (K-major) x K (K-major)
 constexpr uint32_t kIdescPV = idesc_bf16(128, 128, 0, 1);  // P (TMEM) x V (MN-major)
@@ -67,6 +68,32 @@ struct TileCursor {
     }
   }
 };
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// 2^x for a pair on the FMA pipe: x = floor + f, 2^f by a cubic fitted for
+// relative error <= 8.6e-5 on [0,1) (far below the bf16 rounding of P).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  const float kRound = 12582912.f;  // 2^23 + 2^22: adding it (round-down) leaves floor(x) in the low bits
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  float2 r;
+  asm("add.rm.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&x)), "l"(0x4B4000004B400000ull));
+  const float2 fl = fadd2(r, make_float2(-kRound, -kRound));
+  const float2 f = fadd2(x, make_float2(-fl.x, -fl.y));
+  float2 p = ffma2(make_float2(0.07706520f, 0.07706520f), f, make_float2(0.22764701f, 0.22764701f));
+  p = ffma2(p, f, make_float2(0.69511634f, 0.69511634f));
+  p = ffma2(p, f, make_float2(1.f, 1.f));
+  // add floor(x) to the exponent field
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(r.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(r.y) << 23)));
+}
 
 __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant__ Sm100Fwd a) {
   extern __shared__ uint8_t smem_raw[];
@@ -250,15 +277,13 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
 #pragma unroll
         for (int j = 0; j < BN; ++j) s[j] = (j < limit) ? s[j] : -INFINITY;
       }
-      float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+      float mx0 = s[0], mx1 = s[1];
 #pragma unroll
-      for (int j = 4; j < BN; j += 4) {
-        mx0 = fmaxf(mx0, s[j]);
-        mx1 = fmaxf(mx1, s[j + 1]);
-        mx2 = fmaxf(mx2, s[j + 2]);
-        mx3 = fmaxf(mx3, s[j + 3]);
+      for (int j = 2; j < BN - 2; j += 4) {  // two chains of 3-input max (FMNMX3)
+        mx0 = fmax3(mx0, s[j], s[j + 1]);
+        mx1 = fmax3(mx1, s[j + 2], s[j + 3]);
       }
-      const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      const float mx = fmax3(mx0, mx1, fmaxf(s[BN - 2], s[BN - 1])) * sl2;
       if (n == 0 && p.first) {
         m_used = (mx == -INFINITY) ? 0.f : mx;
       } else if (n == 0) {
@@ -310,18 +335,24 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
         }
       }
       if (lane == 0 && wq == 0) TR(6 + 3 * t, n);
-      const float neg_m = -m_used;
-      float ls0 = 0.f, ls1 = 0.f;
-      // P packed in place over the first 64 registers of r[] (r[j/2] <- (p_j, p_j+1))
+      // P = exp2(s tau log2e - m) packed in place over r[0..63]; packed FP32x2 math,
+      // 1 of every kEmuEvery pairs through a cubic on the FMA pipe (MUFU relief)
+      const float2 nm2 = make_float2(-m_used, -m_used);
+      const float2 sl22 = make_float2(sl2, sl2);
+      float2 ls = make_float2(0.f, 0.f);
 #pragma unroll
       for (int j = 0; j < BN; j += 2) {
-        const float e0 = ex2(fmaf(s[j], sl2, neg_m));
-        const float e1 = ex2(fmaf(s[j + 1], sl2, neg_m));
-        ls0 += e0;
-        ls1 += e1;
-        r[j >> 1] = pack_bf16(e0, e1);
+        const float2 x = ffma2(make_float2(s[j], s[j + 1]), sl22, nm2);
+        float2 e;
+        if ((j >> 1) % kEmuEvery == kEmuEvery - 1) {
+          e = ex2_poly2(x);
+        } else {
+          e = make_float2(ex2(x.x), ex2(x.y));
+        }
+        ls = fadd2(ls, e);
+        r[j >> 1] = pack_bf16(e.x, e.y);
       }
-      l += ls0 + ls1;
+      l += ls.x + ls.y;
       tmem_st32(sS + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
       tmem_st32(sS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
       tmem_wait_st();
