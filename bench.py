@@ -51,6 +51,18 @@ def load_peaks():
     return dict(burst=1590.0, sustained=1400.0, hbm=6650.0, source="B200_PROFILING.md fallback")
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
+    --set full capture (profiles/r01/ncu_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))[kernel]
+        return {"bytes": d["dram_read_bytes"] + d["dram_write_bytes"], "launch": d["launch"],
+                "source": "profiles/r01/ncu_traffic.json (ncu --set full, one launch)"}
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
@@ -325,7 +337,7 @@ def run_ours(args, cfg, ws, rank, local):
         "fwd_tflops": round(ach_fwd, 2), "bwd_tflops": round(ach_bwd, 2),
         "roofline": {"bound": "tensor", "kernel": "bwd_kernel (sppo_attn_bwd calls, incl. Delta/cast helpers)",
                      "achieved": round(ach_bwd, 2), "peak": peaks["sustained"], "unit": "TFLOP/s",
-                     "frac": round(ach_bwd / peaks["sustained"], 3), "traffic": None,
+                     "frac": round(ach_bwd / peaks["sustained"], 3), "traffic": ncu_traffic("bwd_kernel"),
                      "peak_kind": "sustained bf16 (kernel timed inside a long step), " + peaks["source"],
                      "share_of_step": round(bwd_ms / ms, 3)},
         "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "offload": offload, "kv_stream": kvs,
