@@ -176,7 +176,8 @@ def run_ours(args, cfg, ws, rank, local):
     dtype = sppo.SPPO_BF16 if cfg["dtype"] == "bf16" else sppo.SPPO_FP32
     tdt = torch.bfloat16 if dtype == sppo.SPPO_BF16 else torch.float32
     ctx = sppo.Context(local)
-    offsets = sppo.partition_equal(S, N)  # a0, in the product's C helper
+    # a0, in the product's C helpers: equal (configs) or FLOPs-balanced
+    offsets = sppo.partition_balanced(S, N) if args.partition == "balanced" else sppo.partition_equal(S, N)
     L = sppo.Layout(h, d, offsets, dtype=dtype)
     x = {t: make_tensor(t, S, heads, d, seed=0, dtype=tdt, device=dev) for t in ("q", "k", "v", "do")}
     eng = engine.ChunkedAttention(ctx, L, device=dev, timing=True)
@@ -256,26 +257,34 @@ def run_ours(args, cfg, ws, rank, local):
         t_fwd = [a.elapsed_time(b) * 1e-3 for a, b in eng.events["fwd"]]
         A = [eng.type1_bytes(i) for i in range(N)]
         thr = [bw * (t_fwd[i + 1] if i + 1 < N else 0.0) for i in range(N)]
-        alpha = sppo.offload_alpha(A, thr, 0.0)
+        alpha = sppo.offload_alpha(A, thr, 0.0)  # sequence-aware (reading L9)
         eng.timing = False
-        res = []
-        moved = None
-        for rep in range(1 + max(1, args.steps // 2)):
-            torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            moved = eng.step_offload(x["q"], x["k"], x["v"], x["do"], alpha, stream)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            if rep > 0:
-                res.append(e0.elapsed_time(e1))
-        off_ms = max_over_ranks(statistics.median(res), ws)
+
+        def time_offload(al):
+            res, moved = [], None
+            for rep in range(1 + max(1, args.steps // 2)):
+                torch.cuda.synchronize()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                moved = eng.step_offload(x["q"], x["k"], x["v"], x["do"], al, stream)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                if rep > 0:
+                    res.append(e0.elapsed_time(e1))
+            return max_over_ranks(statistics.median(res), ws), moved
+
+        off_ms, moved = time_offload(alpha)
+        fix_ms, fix_moved = time_offload([1.0] * (N - 1) + [0.0])  # fixed full offload (P:250 baseline policy)
         offload = {"policy": "type1-alpha (Q,O,LSE offloaded after fwd(i), prefetched depth 2 before bwd(i))",
                    "ms_per_step": round(off_ms, 3), "resident_ms_per_step": round(ms, 3),
                    "exposed_pct": round(100.0 * (off_ms - ms) / ms, 2),
                    "d2h_bytes": moved["d2h"], "h2d_bytes": moved["h2d"],
-                   "alpha": [round(a, 3) for a in alpha], "bw_d2h_gbs_assumed": bw / 1e9}
+                   "alpha": [round(a, 3) for a in alpha], "bw_d2h_gbs_assumed": bw / 1e9,
+                   "fixed_alpha1": {"ms_per_step": round(fix_ms, 3), "exposed_pct": round(100.0 * (fix_ms - ms) / ms, 2),
+                                    "d2h_bytes": fix_moved["d2h"]},
+                   "fwd_ms_per_chunk": [round(t * 1e3, 3) for t in t_fwd],
+                   "d2h_ms_per_chunk_alpha1": [round(a / bw * 1e3, 3) for a in A]}
         eng.free_host()
 
     # ---- KV streaming policy (hot prefix resident, colder chunks streamed from host)
@@ -326,7 +335,8 @@ def run_ours(args, cfg, ws, rank, local):
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
         "config": {"workload": cfg["workload"], "heads": cfg["heads"], "heads_per_gpu": h, "head_dim": d,
-                   "seq_len": S, "chunks": N, "chunk_len": S // N, "policy": "resident (KV + activations on GPU)",
+                   "seq_len": S, "chunks": N, "chunk_len": S // N if args.partition == "equal" else "balanced",
+                   "partition": args.partition, "policy": "resident (KV + activations on GPU)",
                    "parallelism": f"heads sharded over {ws} GPU(s), no collective in step",
                    "l2": f"inputs {4 * S * h * d * eng.elem / 2**30:.1f} GiB per GPU > 126 MB L2 (no flush needed)"},
         "per_gpu_tflops": round(per_gpu, 2),
@@ -380,6 +390,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--kv-hot", type=int, default=-1, help="also time KV streaming with this hot prefix (-1: skip)")
     ap.add_argument("--kv-window", type=int, default=4)
+    ap.add_argument("--partition", default="equal", choices=["equal", "balanced"])
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: warmup < 3 violates the timing rules", file=sys.stderr)

@@ -200,6 +200,11 @@ sppo_status sppo_kv_prefetch(sppo_ctx ctx, int32_t chunk, const void* host, void
 
 /* Equal partition: N+1 offsets, first S mod N chunks longer. */
 sppo_status sppo_partition_equal(int64_t S, int32_t N, int64_t* offsets_out);
+/* FLOPs-balanced partition (P:253, P:256, P:327 [§3.2, §4]): the N
+ * chunks minimising the largest per-chunk causal pair count (attention FLOPs),
+ * ties broken toward longer leading chunks (lengths come out non-increasing).
+ * Writes N+1 offsets.  O(N log^2 S). */
+sppo_status sppo_partition_balanced(int64_t S, int32_t N, int64_t* offsets_out);
 /* Causal (q,k) pairs of all chunks: sum_i s_i c_i + s_i (s_i + 1) / 2. */
 sppo_status sppo_causal_pairs(const int64_t* offsets, int32_t N, int64_t* pairs_out);
 /* Sequence-aware offload ratio (P:371-377 [§5.2]; reading L9):

@@ -39,6 +39,7 @@ from .plan import (  # noqa: F401
     total_pairs,
     attention_flops,
     partition_equal,
+    partition_min_max_pairs,
     offsets_from_lengths,
     offload_alpha,
     memory_timeline,

@@ -47,6 +47,43 @@ def partition_equal(S: int, N: int):
     return [base + (1 if i < rem else 0) for i in range(N)]
 
 
+def partition_min_max_pairs(S: int, N: int):
+    """FLOPs-balanced partition (P:253, P:256, P:327 [§3.2, §4]):
+    the N chunk lengths minimising max_i causal_pairs(s_i, c_i), by exact dynamic
+    programming over split points (small S only).  Among optimal partitions the
+    lexicographically largest length vector is returned ("ties broken toward the
+    longer first chunk").  Cost of a chunk [a, b) is T(b) - T(a) with
+    T(x) = x (x + 1) / 2 (the causal pairs of rows a..b-1)."""
+    if not (1 <= N <= S):
+        raise ValueError("1 <= N <= S required")
+    T = lambda x: x * (x + 1) // 2
+    INF = float("inf")
+    # best[k][e] = min over partitions of [0, e) into k chunks of the max chunk cost
+    best = [[INF] * (S + 1) for _ in range(N + 1)]
+    best[0][0] = 0
+    for k in range(1, N + 1):
+        for e in range(k, S + 1):
+            best[k][e] = min(max(best[k - 1][a], T(e) - T(a)) for a in range(k - 1, e))
+    opt = best[N][S]
+    # reconstruct the lexicographically largest lengths achieving opt: walk forward,
+    # taking each chunk as long as possible while the rest stays feasible.
+    # feasible(k, a) := the suffix [a, S) splits into k chunks each of cost <= opt
+    from functools import lru_cache
+
+    @lru_cache(maxsize=None)
+    def feasible(k, a):
+        if k == 0:
+            return a == S
+        return any(T(b) - T(a) <= opt and feasible(k - 1, b) for b in range(a + 1, S - k + 2))
+
+    lengths, a = [], 0
+    for k in range(N, 0, -1):
+        b = max(b for b in range(a + 1, S - k + 2) if T(b) - T(a) <= opt and feasible(k - 1, b))
+        lengths.append(b - a)
+        a = b
+    return lengths
+
+
 def offsets_from_lengths(lengths):
     """c_0 = 0, c_{i+1} = c_i + s_i (S:105-109)."""
     out = [0]

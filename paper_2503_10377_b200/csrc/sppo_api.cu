@@ -582,6 +582,64 @@ sppo_status sppo_partition_equal(int64_t S, int32_t N, int64_t* out) {
   return SPPO_OK;
 }
 
+namespace {
+int64_t tri(int64_t x) { return x * (x + 1) / 2; }  // causal pairs of rows 0..x-1
+
+// Largest b in (a, S] with tri(b) - tri(a) <= B (a itself if none).
+int64_t greedy_end(int64_t a, int64_t S, int64_t B) {
+  int64_t lo = a, hi = S;
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo + 1) / 2;
+    if (tri(mid) - tri(a) <= B)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+// Chunks a greedy cover of [0, S) needs when no chunk may exceed B pairs (INT64_MAX if impossible).
+int64_t chunks_needed(int64_t S, int64_t B) {
+  int64_t a = 0, n = 0;
+  while (a < S) {
+    const int64_t b = greedy_end(a, S, B);
+    if (b == a) return INT64_MAX;
+    a = b;
+    ++n;
+  }
+  return n;
+}
+}  // namespace
+
+sppo_status sppo_partition_balanced(int64_t S, int32_t N, int64_t* out) {
+  if (!out) return fail(SPPO_E_ARG, "out is NULL");
+  if (N < 1 || S < N || S > (int64_t)INT32_MAX) return fail(SPPO_E_SHAPE, "need 1 <= N <= S < 2^31");
+  // smallest achievable max-chunk cost B*: binary search on the greedy cover count
+  int64_t lo = S, hi = tri(S);  // the last row alone costs S pairs
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (chunks_needed(S, mid) <= N)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  const int64_t B = lo;
+  // lexicographically largest lengths with every chunk <= B and exactly N chunks:
+  // each chunk as long as the cost bound allows, leaving >= 1 row per remaining chunk
+  out[0] = 0;
+  int64_t a = 0;
+  for (int32_t i = 0; i < N; ++i) {
+    const int64_t remaining = N - i - 1;
+    int64_t b = greedy_end(a, S, B);
+    if (b > S - remaining) b = S - remaining;
+    if (b <= a) return fail(SPPO_E_SHAPE, "balanced partition failed (S=%lld, N=%d)", (long long)S, N);
+    out[i + 1] = b;
+    a = b;
+  }
+  if (out[N] != S) return fail(SPPO_E_SHAPE, "balanced partition does not cover S (S=%lld, N=%d)", (long long)S, N);
+  return SPPO_OK;
+}
+
 sppo_status sppo_causal_pairs(const int64_t* off, int32_t N, int64_t* pairs) {
   if (!off || !pairs) return fail(SPPO_E_ARG, "NULL argument");
   if (N < 1) return fail(SPPO_E_SHAPE, "N < 1");

@@ -27,7 +27,7 @@ STATUS = {0: "SPPO_OK", 1: "SPPO_E_ARG", 2: "SPPO_E_SHAPE", 3: "SPPO_E_ALIGN", 4
 # every symbol include/sppo.h declares
 EXPORTS = ("sppo_ctx_create", "sppo_ctx_destroy", "sppo_ctx_sync", "sppo_last_error", "sppo_version",
            "sppo_attn_fwd", "sppo_attn_bwd", "sppo_host_alloc", "sppo_host_free", "sppo_kv_offload",
-           "sppo_kv_prefetch", "sppo_partition_equal", "sppo_causal_pairs", "sppo_offload_alpha")
+           "sppo_kv_prefetch", "sppo_partition_equal", "sppo_partition_balanced", "sppo_causal_pairs", "sppo_offload_alpha")
 
 
 class SppoError(RuntimeError):
@@ -76,6 +76,7 @@ def _load():
         "sppo_kv_offload": ([vp, i32, vp, vp, sz, C.c_double, vp, vp, C.POINTER(sz)], i32),
         "sppo_kv_prefetch": ([vp, i32, vp, vp, sz, vp, vp, i32], i32),
         "sppo_partition_equal": ([C.c_int64, i32, C.POINTER(C.c_int64)], i32),
+        "sppo_partition_balanced": ([C.c_int64, i32, C.POINTER(C.c_int64)], i32),
         "sppo_causal_pairs": ([C.POINTER(C.c_int64), i32, C.POINTER(C.c_int64)], i32),
         "sppo_offload_alpha": ([C.POINTER(C.c_double), C.POINTER(C.c_double), i32, C.c_double,
                                 C.POINTER(C.c_double)], i32),
@@ -133,6 +134,12 @@ def _event(e):
 def partition_equal(S: int, N: int):
     out = (C.c_int64 * (N + 1))()
     _check(_lib.sppo_partition_equal(S, N, out))
+    return list(out)
+
+
+def partition_balanced(S: int, N: int):
+    out = (C.c_int64 * (N + 1))()
+    _check(_lib.sppo_partition_balanced(S, N, out))
     return list(out)
 
 

@@ -77,6 +77,34 @@ def test_kv_stream_matches_oracle(ctx, hot, window):
     eng.free_host()
 
 
+def test_balanced_partition_step_matches_oracle(ctx):
+    """FLOPs-balanced (non-increasing, non-tile-multiple) chunks through the
+    bf16 kernels, full fwd+bwd vs the dense oracle; plus the sequence-aware alpha
+    offload on the same partition (bitwise round trip of O)."""
+    from paper_2503_10377_b200 import engine, sppo
+    S, h, N = 3000, 2, 5
+    off = sppo.partition_balanced(S, N)
+    assert off == oracle.offsets_from_lengths(oracle.partition_min_max_pairs(S, N))
+    x = make_inputs(S, range(h), 128, seed=31, dtype=torch.bfloat16)
+    dev = {k: v.cuda() for k, v in x.items()}
+    eng = engine.ChunkedAttention(ctx, sppo.Layout(h, 128, off))
+    eng.step(dev["q"], dev["k"], dev["v"], dev["do"])
+    torch.cuda.synchronize()
+    o_ref = eng.o.clone()
+    xn = {kk: vv.double().numpy() for kk, vv in x.items()}
+    ref = oracle.causal_attention_dense_bwd(xn["q"], xn["k"], xn["v"], xn["do"])
+    np.testing.assert_allclose(eng.o.double().cpu().numpy(), ref["o"], **O_TOL)
+    for key in ("dq", "dk", "dv"):
+        np.testing.assert_allclose(getattr(eng, key).double().cpu().numpy(), ref[key], **G_TOL, err_msg=key)
+    A = [eng.type1_bytes(i) for i in range(N)]
+    alpha = sppo.offload_alpha(A, [A[-1]] * N, 0.0)  # constant M_threshold = the smallest chunk (P:377)
+    assert alpha == oracle.offload_alpha(A, [A[-1]] * N, 0.0) and alpha[0] < 1.0
+    eng.step_offload(dev["q"].clone(), dev["k"], dev["v"], dev["do"], alpha, poison=True)
+    torch.cuda.synchronize()
+    assert torch.equal(eng.o, o_ref)
+    eng.free_host()
+
+
 def test_alpha_planner_in_engine_matches_oracle(ctx):
     """The bench's alpha: per-chunk M_i = BW * T_fwd(i+1) from measured forward
     times; the product's sppo_offload_alpha and the oracle agree."""
