@@ -38,6 +38,8 @@ CONFIGS = {
                workload="configs[2] GPT-7B shape: 32 heads, d=128, S=1M, N=64, bf16"),
     "C4": dict(heads=40, d=128, S=524288, N=32, dtype="bf16",
                workload="configs[3] GPT-13B shape: 40 heads, d=128, S=512K, N=32, bf16"),
+    "C5": dict(heads=64, d=128, S=4194304, N=256, dtype="bf16",
+               workload="configs[4] GPT-65B shape: 64 heads, d=128, S=4M, N=256, bf16"),
 }
 METRIC = "chunked attn fwd+bwd TFLOP/s per B200 (% BF16 peak), tokens/s at 1/2/4/8 GPU"
 
@@ -139,9 +141,13 @@ def dist_setup():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test-only overrides: run several ranks on one GPU (SPPO_BENCH_DEVICE=0) over gloo
+    # (SPPO_DIST_BACKEND=gloo) to exercise the multi-rank path where only one GPU exists
+    if "SPPO_BENCH_DEVICE" in os.environ:
+        local = int(os.environ["SPPO_BENCH_DEVICE"])
     if ws > 1:
         import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        backend = os.environ.get("SPPO_DIST_BACKEND", "nccl" if torch.cuda.is_available() else "gloo")
         if torch.cuda.is_available():
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
@@ -171,7 +177,10 @@ def run_ours(args, cfg, ws, rank, local):
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    heads = head_range(cfg["heads"], ws, rank)
+    # --shard-of G: run rank 0's share of a G-GPU head split on this one GPU (per-GPU
+    # measurement of a config that needs G GPUs; value is then per GPU, not aggregate)
+    shard = args.shard_of if ws == 1 else ws
+    heads = head_range(cfg["heads"], shard, rank)
     h, d, S, N = len(heads), cfg["d"], cfg["S"], cfg["N"]
     dtype = sppo.SPPO_BF16 if cfg["dtype"] == "bf16" else sppo.SPPO_FP32
     tdt = torch.bfloat16 if dtype == sppo.SPPO_BF16 else torch.float32
@@ -207,7 +216,7 @@ def run_ours(args, cfg, ws, rank, local):
     bwd_ms = eng.kernel_ms("bwd") / args.steps
 
     fl_dev = flops_of(offsets, h, d)
-    fl_total = flops_of(offsets, cfg["heads"], d)
+    fl_total = flops_of(offsets, cfg["heads"] if args.shard_of == 1 else len(heads), d)
     peaks = load_peaks()
     tflops = fl_total / (ms * 1e-3) / 1e12
     per_gpu = tflops / ws
@@ -318,7 +327,8 @@ def run_ours(args, cfg, ws, rank, local):
         g0 = time.perf_counter()
         full = gather_heads(eng.o, ws)
         torch.cuda.synchronize()
-        gather = {"op": "all_gather_into_tensor(O) over NCCL", "ms": round((time.perf_counter() - g0) * 1e3, 2),
+        import torch.distributed as dist
+        gather = {"op": f"all_gather O over {dist.get_backend()}", "ms": round((time.perf_counter() - g0) * 1e3, 2),
                   "bytes": full.numel() * full.element_size()}
 
     cpu = None
@@ -337,7 +347,9 @@ def run_ours(args, cfg, ws, rank, local):
         "config": {"workload": cfg["workload"], "heads": cfg["heads"], "heads_per_gpu": h, "head_dim": d,
                    "seq_len": S, "chunks": N, "chunk_len": S // N if args.partition == "equal" else "balanced",
                    "partition": args.partition, "policy": "resident (KV + activations on GPU)",
-                   "parallelism": f"heads sharded over {ws} GPU(s), no collective in step",
+                   "parallelism": (f"heads sharded over {ws} GPU(s), no collective in step" if args.shard_of == 1 else
+                                   f"rank 0's share of a {args.shard_of}-GPU head split, run on 1 GPU "
+                                   f"(value = per-GPU TFLOP/s of that config)"),
                    "l2": f"inputs {4 * S * h * d * eng.elem / 2**30:.1f} GiB per GPU > 126 MB L2 (no flush needed)"},
         "per_gpu_tflops": round(per_gpu, 2),
         "pct_bf16_peak": {"burst": round(100 * per_gpu / peaks["burst"], 1),
@@ -391,6 +403,7 @@ def main():
     ap.add_argument("--kv-hot", type=int, default=-1, help="also time KV streaming with this hot prefix (-1: skip)")
     ap.add_argument("--kv-window", type=int, default=4)
     ap.add_argument("--partition", default="equal", choices=["equal", "balanced"])
+    ap.add_argument("--shard-of", type=int, default=1, help="1 GPU: run rank 0's heads of a G-GPU split")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: warmup < 3 violates the timing rules", file=sys.stderr)

@@ -28,6 +28,8 @@ def max_over_ranks(x: float, world: int, device=None) -> float:
     if world == 1:
         return float(x)
     import torch.distributed as dist
+    if dist.get_backend() != "nccl":
+        device = "cpu"
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -40,7 +42,12 @@ def gather_heads(local: torch.Tensor, world: int) -> torch.Tensor:
         return local
     import torch.distributed as dist
     local = local.contiguous()
+    if dist.get_backend() != "nccl":  # gloo (CPU tests): gather host copies
+        local = local.cpu()
     parts = torch.empty((world,) + tuple(local.shape), dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(parts, local) if local.is_cuda else dist.all_gather(list(parts.unbind(0)), local)
+    if local.is_cuda:
+        dist.all_gather_into_tensor(parts, local)  # NCCL over NVLink / NVSwitch
+    else:
+        dist.all_gather(list(parts.unbind(0)), local)
     # [G, S, h/G, d] -> [S, G*h/G, d]
     return parts.permute(1, 0, 2, 3).reshape(local.shape[0], world * local.shape[1], local.shape[2])
