@@ -8,7 +8,7 @@ lib = ctypes.CDLL(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(_
 lib.tc_mma_bench.restype = ctypes.c_longlong
 names = {0: "SS  A K-major,  B K-major ", 1: "SS  A K-major,  B MN-major", 2: "TS  A TMEM,     B MN-major",
          3: "SS  A MN-major, B MN-major", 4: "SS  A MN-major, B K-major "}
-for N in (128,):
+for N in (128, 64):
     for mode in range(5):
         for zero in (0, 10):
             lib.tc_mma_bench(mode + zero, N, 10)
