@@ -46,7 +46,7 @@ struct Bars {
   uint64_t k_full[2], k_empty[2];
   uint64_t v_full[2], v_empty[2];
   uint64_t s_full[2];   // S_t ready in TMEM (per Q tile)
-  uint64_t p_full[2];   // P_t written to TMEM (128 softmax threads arrive)
+  uint64_t p_full[2][2];  // P_t keys [64h, 64h+64) written to TMEM (128 softmax threads arrive)
   uint64_t o_full[2];   // PV_t complete
   uint32_t tmem_base;
 };
@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       mbar_init(&bars.v_full[s], 1);
       mbar_init(&bars.v_empty[s], 1);
       mbar_init(&bars.s_full[s], 1);
-      mbar_init(&bars.p_full[s], 128);
+      mbar_init(&bars.p_full[s][0], 128);
+      mbar_init(&bars.p_full[s][1], 128);
       mbar_init(&bars.o_full[s], 1);
     }
     fence_mbar_init();
@@ -204,12 +205,19 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
         }
         mma_commit_w(&bars.s_full[t]);
       };
+      // O_t += P_t V in two K-halves: the first 64 keys go as soon as the softmax has
+      // written them, overlapping the exponentials of the second half
       auto issue_pv = [&](int t, int stage, int n) {
         const uint64_t va = dV0 + stage * kStep;
 #pragma unroll
-        for (int k = 0; k < BN / 16; ++k)
-          mma_ts_w(tO[t], tS[t] + k * 8, va + ((k * 2048) >> 4), kIdescPV,
-                   (n > 0 || k > 0 || !p.first) ? 1u : 0u);  // !first: O holds the carried-in state
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(&bars.p_full[t][h], n & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 4 * h; k < 4 * h + 4; ++k)
+            mma_ts_w(tO[t], tS[t] + k * 8, va + ((k * 2048) >> 4), kIdescPV,
+                     (n > 0 || k > 0 || !p.first) ? 1u : 0u);  // !first: O holds the carried-in state
+        }
         mma_commit_w(&bars.o_full[t]);
       };
       mbar_wait(&bars.q_full, 0);
@@ -228,8 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
           if (n < T[t]) {
-            mbar_wait(&bars.p_full[t], n & 1);
-            tc_fence_after();
+
             TR(1 + 2 * t, n);
             issue_pv(t, vs, n);
             if (nx < T[t]) {
@@ -341,24 +348,26 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       const float2 sl22 = make_float2(sl2, sl2);
       float2 ls = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int j = 0; j < BN; j += 2) {
-        const float2 x = ffma2(make_float2(s[j], s[j + 1]), sl22, nm2);
-        float2 e;
-        if ((j >> 1) % kEmuEvery == kEmuEvery - 1) {
-          e = ex2_poly2(x);
-        } else {
-          e = make_float2(ex2(x.x), ex2(x.y));
+      for (int h = 0; h < 2; ++h) {  // two 64-key halves, each handed to the MMA warp when done
+#pragma unroll
+        for (int j = 64 * h; j < 64 * h + 64; j += 2) {
+          const float2 x = ffma2(make_float2(s[j], s[j + 1]), sl22, nm2);
+          float2 e;
+          if ((j >> 1) % kEmuEvery == kEmuEvery - 1) {
+            e = ex2_poly2(x);
+          } else {
+            e = make_float2(ex2(x.x), ex2(x.y));
+          }
+          ls = fadd2(ls, e);
+          r[j >> 1] = pack_bf16(e.x, e.y);
         }
-        ls = fadd2(ls, e);
-        r[j >> 1] = pack_bf16(e.x, e.y);
+        tmem_st32(sS + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(&r[32 * h]));
+        tmem_wait_st();
+        tc_fence_before();
+        if (h == 1 && lane == 0 && wq == 0) TR(7 + 3 * t, n);
+        mbar_arrive(&bars.p_full[t][h]);
       }
       l += ls.x + ls.y;
-      tmem_st32(sS + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-      tmem_st32(sS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-      tmem_wait_st();
-      tc_fence_before();
-      if (lane == 0 && wq == 0) TR(7 + 3 * t, n);
-      mbar_arrive(&bars.p_full[t]);
     }
     if (Tt > 0) {
       mbar_wait(&bars.o_full[t], (Tt - 1) & 1);
