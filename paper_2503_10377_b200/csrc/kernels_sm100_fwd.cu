@@ -271,6 +271,9 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       const int valid = min(BN, a.len[cur.c] - cur.tt * BN);
       const int limit = min(valid, pos - kpos0 + 1);  // columns >= limit are masked
       mbar_wait(&bars.s_full[t], n & 1);
+      // PV(n-1) completed before S(n) (same issuing thread, in-order pipe): consuming its
+      // o_full phase here is free and keeps every mbarrier phase waited on (synccheck-clean)
+      if (n > 0) mbar_wait(&bars.o_full[t], (n - 1) & 1);
       if (lane == 0 && wq == 0) TR(5 + 3 * t, n);
       tc_fence_after();
       uint32_t r[128];
@@ -327,8 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
             m_used = mx;
             l *= f;
           }
-          mbar_wait(&bars.o_full[t], (n - 1) & 1);  // PV(n-1) finished writing O
-          tc_fence_after();
+          // PV(n-1) finished writing O (waited above)
 #pragma unroll
           for (int cb = 0; cb < 4; ++cb) {
             uint32_t o[32];
