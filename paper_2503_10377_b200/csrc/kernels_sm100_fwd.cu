@@ -264,6 +264,31 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     const uint32_t sS = tS[t] + lane_off, sO = tO[t] + lane_off;
     float m_used = -INFINITY, l = 0.f;
+    if (!p.first && T[t] > 0) {
+      // carry-in of an earlier window: natural-log m, l and the
+      // unnormalised o_acc row go straight into O / the running state; the first
+      // tile then proceeds like any later one (speculative exps + rescale check)
+      const bool ok = row < p.q_len;
+      const size_t vi = (size_t)head * p.q_len + row;
+      const float m_in = ok ? p.m[vi] * kLog2e : -INFINITY;
+      m_used = (m_in == -INFINITY) ? 0.f : m_in;
+      l = ok ? p.l[vi] : 0.f;
+      const float4* src = reinterpret_cast<const float4*>(p.o_acc + ((size_t)row * p.heads + head) * HD);
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) {
+        uint32_t o[32];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const float4 x = ok ? src[cb * 8 + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+          o[4 * v + 0] = __float_as_uint(x.x);
+          o[4 * v + 1] = __float_as_uint(x.y);
+          o[4 * v + 2] = __float_as_uint(x.z);
+          o[4 * v + 3] = __float_as_uint(x.w);
+        }
+        tmem_st32(sO + cb * 32, o);
+      }
+      tmem_wait_st();
+    }
     const int Tt = T[t];
     TileCursor cur;
     for (int n = 0; n < Tt; ++n, cur.next(a)) {
@@ -277,52 +302,67 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       if (lane == 0 && wq == 0) TR(5 + 3 * t, n);
       tc_fence_after();
       uint32_t r[128];
-      tmem_ld32(sS + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-      tmem_ld32(sS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-      tmem_ld32(sS + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
-      tmem_ld32(sS + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
-      tmem_wait_ld();
+      auto R32 = [&](int c) -> uint32_t(&)[32] { return *reinterpret_cast<uint32_t(*)[32]>(&r[c]); };
+      // keys 0..63 first; on unmasked later tiles keys 64..127 keep loading while the
+      // first 64 exponentials run (split load), otherwise everything is loaded up front
+      const bool split = !(n == 0 && p.first) && __all_sync(0xffffffffu, limit >= BN);
+      tmem_ld32(sS + 0, R32(0));
+      tmem_ld32(sS + 32, R32(32));
+      tmem_wait_ld_regs(R32(0));
+      tmem_wait_ld_regs(R32(32));
+      tmem_ld32(sS + 64, R32(64));
+      tmem_ld32(sS + 96, R32(96));
+      if (!split) {
+        tmem_wait_ld_regs(R32(64));
+        tmem_wait_ld_regs(R32(96));
+      }
       float* s = reinterpret_cast<float*>(r);
       if (limit < BN) {
 #pragma unroll
         for (int j = 0; j < BN; ++j) s[j] = (j < limit) ? s[j] : -INFINITY;
       }
-      float mx0 = s[0], mx1 = s[1];
+      auto row_max = [&]() {
+        float mx0 = s[0], mx1 = s[1];
 #pragma unroll
-      for (int j = 2; j < BN - 2; j += 4) {  // two chains of 3-input max (FMNMX3)
-        mx0 = fmax3(mx0, s[j], s[j + 1]);
-        mx1 = fmax3(mx1, s[j + 2], s[j + 3]);
-      }
-      const float mx = fmax3(mx0, mx1, fmaxf(s[BN - 2], s[BN - 1])) * sl2;
-      if (n == 0 && p.first) {
-        m_used = (mx == -INFINITY) ? 0.f : mx;
-      } else if (n == 0) {
-        // carry-in of an earlier window: natural-log m, l and the
-        // unnormalised o_acc row, rescaled to the merged max and written into O
-        const bool ok = row < p.q_len;
-        const size_t vi = (size_t)head * p.q_len + row;
-        const float m_in = ok ? p.m[vi] * kLog2e : -INFINITY;
-        const float l_in = ok ? p.l[vi] : 0.f;
-        m_used = fmaxf(m_in, mx);
-        if (m_used == -INFINITY) m_used = 0.f;
-        const float f = (m_in == -INFINITY) ? 0.f : ex2(m_in - m_used);
-        l = l_in * f;
-        const float4* src = reinterpret_cast<const float4*>(p.o_acc + ((size_t)row * p.heads + head) * HD);
-#pragma unroll
-        for (int cb = 0; cb < 4; ++cb) {
-          uint32_t o[32];
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            const float4 x = ok ? src[cb * 8 + v] : make_float4(0.f, 0.f, 0.f, 0.f);
-            o[4 * v + 0] = __float_as_uint(x.x * f);
-            o[4 * v + 1] = __float_as_uint(x.y * f);
-            o[4 * v + 2] = __float_as_uint(x.z * f);
-            o[4 * v + 3] = __float_as_uint(x.w * f);
-          }
-          tmem_st32(sO + cb * 32, o);
+        for (int j = 2; j < BN - 2; j += 4) {  // two chains of 3-input max (FMNMX3)
+          mx0 = fmax3(mx0, s[j], s[j + 1]);
+          mx1 = fmax3(mx1, s[j + 2], s[j + 3]);
         }
-        tmem_wait_st();
+        return fmax3(mx0, mx1, fmaxf(s[BN - 2], s[BN - 1])) * sl2;
+      };
+      // P = exp2(s tau log2e - m) for 64 keys from j0, bf16 pairs into out[]; packed
+      // FP32x2 math, 1 of every kEmuEvery pairs through a cubic on the FMA pipe
+      auto exps = [&](int j0, float negm, uint32_t* out, float2& lsum) {
+        const float2 nm2 = make_float2(negm, negm);
+        const float2 sl22 = make_float2(sl2, sl2);
+#pragma unroll
+        for (int j = j0; j < j0 + 64; j += 2) {
+          const float2 x = ffma2(make_float2(s[j], s[j + 1]), sl22, nm2);
+          float2 e;
+          if ((j >> 1) % kEmuEvery == kEmuEvery - 1) {
+            e = ex2_poly2(x);
+          } else {
+            e = make_float2(ex2(x.x), ex2(x.y));
+          }
+          lsum = fadd2(lsum, e);
+          out[(j - j0) >> 1] = pack_bf16(e.x, e.y);
+        }
+      };
+      uint32_t pk0[32];
+      float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
+      if (n == 0 && p.first) {
+        const float mx = row_max();
+        m_used = (mx == -INFINITY) ? 0.f : mx;
+        exps(0, -m_used, pk0, ls0);
       } else {
+        // speculative: the first 64 exponentials run against the stale max m_used
+        // while the row max is computed alongside; only a (rare) rescale redoes them
+        exps(0, -m_used, pk0, ls0);
+        if (split) {
+          tmem_wait_ld_regs(R32(64));
+          tmem_wait_ld_regs(R32(96));
+        }
+        const float mx = row_max();
         const bool need = mx > m_used + kRescaleThreshold;
         if (__any_sync(0xffffffffu, need)) {
           const float f = need ? ex2(m_used - mx) : 1.f;
@@ -341,35 +381,22 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
             tmem_st32(sO + cb * 32, o);
           }
           tmem_wait_st();
+          ls0 = make_float2(0.f, 0.f);
+          exps(0, -m_used, pk0, ls0);
         }
       }
       if (lane == 0 && wq == 0) TR(6 + 3 * t, n);
-      // P = exp2(s tau log2e - m) packed in place over r[0..63]; packed FP32x2 math,
-      // 1 of every kEmuEvery pairs through a cubic on the FMA pipe (MUFU relief)
-      const float2 nm2 = make_float2(-m_used, -m_used);
-      const float2 sl22 = make_float2(sl2, sl2);
-      float2 ls = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {  // two 64-key halves, each handed to the MMA warp when done
-#pragma unroll
-        for (int j = 64 * h; j < 64 * h + 64; j += 2) {
-          const float2 x = ffma2(make_float2(s[j], s[j + 1]), sl22, nm2);
-          float2 e;
-          if ((j >> 1) % kEmuEvery == kEmuEvery - 1) {
-            e = ex2_poly2(x);
-          } else {
-            e = make_float2(ex2(x.x), ex2(x.y));
-          }
-          ls = fadd2(ls, e);
-          r[j >> 1] = pack_bf16(e.x, e.y);
-        }
-        tmem_st32(sS + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(&r[32 * h]));
-        tmem_wait_st();
-        tc_fence_before();
-        if (h == 1 && lane == 0 && wq == 0) TR(7 + 3 * t, n);
-        mbar_arrive(&bars.p_full[t][h]);
-      }
-      l += ls.x + ls.y;
+      tmem_st32(sS + 0, pk0);  // P keys 0..63 -> the MMA warp starts PV's first half
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&bars.p_full[t][0]);
+      exps(64, -m_used, &r[32], ls1);  // keys 64..127 packed over r[32..63] (already consumed)
+      tmem_st32(sS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+      tmem_wait_st();
+      tc_fence_before();
+      if (lane == 0 && wq == 0) TR(7 + 3 * t, n);
+      mbar_arrive(&bars.p_full[t][1]);
+      l += ls0.x + ls0.y + ls1.x + ls1.y;
     }
     if (Tt > 0) {
       mbar_wait(&bars.o_full[t], (Tt - 1) & 1);

@@ -1,0 +1,3 @@
+timeout 300 python -m pytest tests/test_gpu_bf16.py tests/test_gpu_policies.py tests/test_gpu_edge.py -q -x -m "not slow" 2>&1 | tail -1
+SPPO_TRACE=gpurun_out/trace_fwd15.txt SPPO_TRACE_CHUNK=15 SPPO_TRACE_KIND=fwd timeout 300 python tools/trace_run.py 2>&1 | grep "median period"
+timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-offload --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print({k:d[k] for k in ('value','ms_per_step','fwd_tflops','bwd_tflops','clocks')})"

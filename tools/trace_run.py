@@ -28,9 +28,10 @@ if kind == "bwd":
     pairs = [(1, 2), (2, 3), (3, 4), (4, 5), (0, 1), (6, 7), (8, 9), (12, 13), (1, 8), (4, 9)]
     period_slot = 2
 else:
-    names = ["-", "PV", "S+2", "-", "-", "sseen", "smax", "pfull", "-", "-", "-", "ldK", "-", "-", "-", "-"]
-    pairs = [(5, 6), (6, 7), (7, 1), (1, 2), (2, 5), (11, 5)]
-    period_slot = 1
+    names = ["vfull", "PV0", "S0+1", "PV1", "S1+1", "s0seen", "s0max", "p0full", "s1seen", "s1max", "p1full",
+             "ldK", "ldV", "-", "-", "-"]
+    pairs = [(5, 6), (6, 7), (8, 9), (9, 10), (1, 2), (3, 4), (7, 2), (10, 4), (2, 5), (4, 8)]
+    period_slot = 2
 base = rows[0][1]
 for r in rows[:4] + rows[len(rows) // 2:len(rows) // 2 + 3]:
     print(r[0], " ".join(f"{n}={(v - base) if v else -1}" for n, v in zip(names, r[1:])))
