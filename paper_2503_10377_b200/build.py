@@ -2,6 +2,7 @@
 
   libsppo.so            — the product: C ABI (include/sppo.h) + all kernels
   tests/cuda/libtcprobe.so — test-only tcgen05/TMA layout probe
+  examples/sppo_c_demo  — examples/sppo_c_demo.c: a step driven from plain C via the ABI
 
 Run ``python -m paper_2503_10377_b200.build`` or ``__graft_entry__.build()``.
 Objects are rebuilt only when a source or header is newer than the object.
@@ -27,6 +28,8 @@ FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--
 LIB = os.path.join(PKG, "libsppo.so")
 PROBE_SRC = os.path.join(ROOT, "tests", "cuda", "tc_probe.cu")
 PROBE_LIB = os.path.join(ROOT, "tests", "cuda", "libtcprobe.so")
+DEMO_SRC = os.path.join(ROOT, "examples", "sppo_c_demo.c")
+DEMO_BIN = os.path.join(ROOT, "examples", "sppo_c_demo")  # not under build/: must ship to the GPU box
 
 
 def _headers():
@@ -72,6 +75,10 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if force or _stale(PROBE_LIB, [PROBE_SRC] + hdrs):
         _run([NVCC] + FLAGS + ["-shared", "-o", PROBE_LIB, PROBE_SRC, "-lcudart", "-Xlinker",
                                "-rpath=/usr/local/cuda/lib64"], PROBE_LIB + ".log")
+    if force or _stale(DEMO_BIN, [DEMO_SRC, LIB, os.path.join(ROOT, "include", "sppo.h")]):
+        _run(["gcc", "-O2", "-std=c11", "-Wall", DEMO_SRC, "-I" + os.path.join(ROOT, "include"),
+              "-I/usr/local/cuda/include", "-L" + PKG, "-lsppo", "-L/usr/local/cuda/lib64", "-lcudart",
+              "-Wl,-rpath," + PKG + ":/usr/local/cuda/lib64", "-lm", "-o", DEMO_BIN])
     if verbose:
         for o in objs:
             log = o + ".log"

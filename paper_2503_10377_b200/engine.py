@@ -352,19 +352,21 @@ class ChunkedAttention:
         N = L.num_chunks
         strm = stream or torch.cuda.current_stream()
         h2d = d2h = 0
-        ready = []
-        for i in range(N):
-            evs = []
-            for name in ("q", "k", "v", "do"):
-                t = self.rows(dev_in[name], i)
-                nb = t.numel() * t.element_size()
-                off = L.offsets[i] * L.heads * L.head_dim * self.elem
-                ev = torch.cuda.Event()
-                self.ctx.kv_prefetch(i, host_in[name] + off, t, nb, consumer=strm, done=ev,
-                                     flags=sppo.SPPO_COPY_NO_ORDER | sppo.SPPO_COPY_DEFER_WAIT)
-                h2d += nb
-                evs.append(ev)
-            ready.append(evs)
+        # Issue order = consumption order on the single H2D stream: Q,K,V chunk by
+        # chunk for the forward, then dO from the last chunk down for the
+        # backward (which runs N-1 .. 0), so no copy queues behind one needed later.
+        ready = [[None] * 4 for _ in range(N)]
+        order = [(i, j, name) for i in range(N) for j, name in enumerate(("q", "k", "v"))]
+        order += [(i, 3, "do") for i in range(N - 1, -1, -1)]
+        for i, j, name in order:
+            t = self.rows(dev_in[name], i)
+            nb = t.numel() * t.element_size()
+            off = L.offsets[i] * L.heads * L.head_dim * self.elem
+            ev = torch.cuda.Event()
+            self.ctx.kv_prefetch(i, host_in[name] + off, t, nb, consumer=strm, done=ev,
+                                 flags=sppo.SPPO_COPY_NO_ORDER | sppo.SPPO_COPY_DEFER_WAIT)
+            h2d += nb
+            ready[i][j] = ev
         self.dk_acc.zero_()
         self.dv_acc.zero_()
         last = None

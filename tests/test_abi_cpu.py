@@ -58,3 +58,17 @@ def test_ctx_without_gpu_fails_loudly():
     with pytest.raises(sppo.SppoError) as e:
         sppo.Context(0)
     assert e.value.name in ("SPPO_E_CUDA", "SPPO_E_ARG")
+
+
+def test_c_demo_links_against_the_abi():
+    """examples/sppo_c_demo (plain C, no torch) is built by build() and links
+    libsppo.so; without a GPU it must fail loudly at sppo_ctx_create."""
+    import subprocess
+    import torch
+    exe = os.path.join(ROOT, "examples", "sppo_c_demo")
+    assert os.path.exists(exe), "run __graft_entry__.build()"
+    ldd = subprocess.run(["ldd", exe], capture_output=True, text=True).stdout
+    assert "libsppo.so" in ldd and "not found" not in ldd, ldd
+    if not torch.cuda.is_available():
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+        assert r.returncode == 1 and "sppo_ctx_create" in r.stderr, r.stderr

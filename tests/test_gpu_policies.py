@@ -113,3 +113,47 @@ def test_alpha_planner_in_engine_matches_oracle(ctx):
     A = [eng.type1_bytes(i) for i in range(4)]
     thr = [1e6, 5e6, 2e7, 0.0]
     assert sppo.offload_alpha(A, thr, 0.0) == oracle.offload_alpha(A, thr, 0.0)
+
+
+def test_host_io_step_matches_resident(ctx):
+    """The e2e path bench.py times (step_host_io): Q, K, V, dO start in pinned
+    host memory, the device input buffers start as NaN, and O, dQ, dK, dV end in
+    pinned host memory.  Same kernels and windows as the resident step, so O,
+    dK, dV are bitwise equal; dQ (reduce-add order) within 1e-2."""
+    import ctypes
+    x, dev, eng = setup(ctx, 2304, 2, 5, seed=24)
+    eng.step(dev["q"], dev["k"], dev["v"], dev["do"])
+    torch.cuda.synchronize()
+    ref = snapshot(eng)
+    nb = dev["q"].numel() * dev["q"].element_size()
+    host_in = {t: ctx.host_alloc(nb) for t in ("q", "k", "v", "do")}
+    host_out = {t: ctx.host_alloc(nb) for t in ("o", "dq", "dk", "dv")}
+    for t in host_in:
+        ctx.kv_offload(0, dev[t], host_in[t], nb)
+    ctx.sync()
+    blank = {t: torch.full_like(dev[t], float("nan")) for t in host_in}
+    h2d, d2h, last = eng.step_host_io(host_in, host_out, blank)
+    last.synchronize()
+    ctx.sync()
+    assert h2d == 4 * nb and d2h == 4 * nb
+    for t in ("o", "dq", "dk", "dv"):
+        buf = (ctypes.c_uint8 * nb).from_address(host_out[t])
+        got = torch.frombuffer(bytearray(buf), dtype=torch.bfloat16).view_as(ref[t])
+        want = ref[t].cpu()
+        if t == "dq":
+            assert (got.float() - want.float()).abs().max().item() < 1e-2
+        else:
+            assert torch.equal(got, want), t
+    for p in list(host_in.values()) + list(host_out.values()):
+        ctx.host_free(p)
+
+
+def test_c_demo_runs():
+    """examples/sppo_c_demo: a whole step (balanced partition, fwd, O offload,
+    NaN overwrite, prefetch, bwd) driven from plain C through the ABI only."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "examples", "sppo_c_demo")
+    for args in ([], ["3000", "5", "3"], ["129", "2", "1"]):
+        r = subprocess.run([exe] + args, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0 and "PASS" in r.stdout, r.stdout + r.stderr
