@@ -86,11 +86,13 @@ struct Sm100Fwd {
 struct Sm100Bwd {
   BwdParams p;
   const void* desc_table;
-  int32_t q_slot, do_slot, dq_slot;  // bf16 Q_i, dO_i maps; fp32 dQ-accumulator map (reduce-add)
+  // bf16 Q_i / dO_i maps with 128-row and 64-row boxes; fp32 dQ-accumulator map
+  // (TMA reduce-add of dQ partial sums)
+  int32_t q_slot, do_slot, q64_slot, do64_slot, dq_slot;
   int32_t n;
   int32_t start[kMaxWindow];
   int32_t len[kMaxWindow];
-  int32_t tile_base[kMaxWindow + 1];  // prefix count of 128-key tiles per window chunk
+  int32_t pair_base[kMaxWindow + 1];  // prefix count of 256-key CTA-pair tiles per window chunk
   TmaSlots slots;
   float* dk[kMaxWindow];
   float* dv[kMaxWindow];

@@ -478,8 +478,10 @@ sppo_status sppo_attn_bwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
     sa.desc_table = ctx->desc_dev;
     if ((s = get_desc(ctx, q, p.q_len, p.heads, p.d, 128, strm, &sa.q_slot))) return s;
     if ((s = get_desc(ctx, a->dout, p.q_len, p.heads, p.d, 128, strm, &sa.do_slot))) return s;
+    if ((s = get_desc(ctx, q, p.q_len, p.heads, p.d, 64, strm, &sa.q64_slot))) return s;
+    if ((s = get_desc(ctx, a->dout, p.q_len, p.heads, p.d, 64, strm, &sa.do64_slot))) return s;
     if ((s = get_desc(ctx, a->dq_acc, p.q_len, p.heads, p.d, 128, strm, &sa.dq_slot, 4))) return s;
-    int tiles = 0;
+    int pairs = 0;
     for (int c = 0; c < kv->n; ++c) {
       int sk, sv;
       if ((s = get_desc(ctx, kv->k[c], w.len[c], p.heads, p.d, 128, strm, &sk))) return s;
@@ -488,12 +490,12 @@ sppo_status sppo_attn_bwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
       sa.slots.v[c] = (uint16_t)sv;
       sa.start[c] = w.start[c];
       sa.len[c] = w.len[c];
-      sa.tile_base[c] = tiles;
-      tiles += (w.len[c] + 127) / 128;
+      sa.pair_base[c] = pairs;
+      pairs += (w.len[c] + 255) / 256;
       sa.dk[c] = g.dk[c];
       sa.dv[c] = g.dv[c];
     }
-    sa.tile_base[kv->n] = tiles;
+    sa.pair_base[kv->n] = pairs;
     e = launch_bwd_sm100(sa, strm);
   }
   if (e == cudaErrorNotSupported) return fail(SPPO_E_UNSUPPORTED, "this request is not implemented by the sm_100a kernels");
