@@ -13,11 +13,12 @@
 //   S^T  = K Q^T      M=256 N=128 K=128  A = own K (smem), B = Q rows [64r,+64)
 //   dP^T = V dO^T     M=256 N=128 K=128  A = own V,        B = dO rows [64r,+64)
 //   dV  += P^T dO     M=256 N=128 K=128  A = P^T (TMEM),   B = dO cols [64r,+64)
-//   dK  += dS^T Q     M=256 N=128 K=128  A = dS^T (TMEM),  B = Q cols [64r,+64)
+//   dK  += dS^T Q     M=256 N=128 K=128  A = dS^T (smem, K-major), B = Q cols [64r,+64)
 // and dQ = dS K (M=N=K=128, A = dS, B = own K, both MN-major smem) is a
-// cta_group::1 MMA each CTA issues for its own keys.  Halving the B reads cuts
-// shared-memory traffic per Q tile from ~480 KB to ~416 KB; the one-CTA-per-
-// key-tile kernel was bound by exactly that (profiles/r01).
+// cta_group::1 MMA each CTA issues for its own keys.  dS lives only in smem
+// ([keys][q]: K-major A of dK and MN-major A of dQ), so dQ(m) is issued before
+// dK(m) and its TMEM readout overlaps dK(m): the per-tile critical chain is
+// dP -> dS -> dQ -> readout -> next dP (all share TMEM region 2).
 // (Pairing dQ too, M=128 over 256 keys, needs half of dS from the peer over
 // DSMEM at ~20 B/clk: measured 3000 cycles per tile slower; not used.)
 // 512 threads per CTA:
@@ -28,7 +29,7 @@
 //   warp 13     TMA: K, V once; Q rows half + LSE per tile
 //   warp 14     TMEM alloc/dealloc; TMA dO columns half + Q columns half per tile
 //   warp 15     TMA: dO rows half + Delta per tile
-// TMEM (512 cols per CTA): S/P [0,128) | dV [128,256) | dP/dS/dQ [256,384) | dK [384,512)
+// TMEM (512 cols per CTA): S/P [0,128) | dV [128,256) | dP/dQ [256,384) | dK [384,512)
 // Operand TMA loads of both CTAs complete on the leader's barriers; MMA commits
 // multicast to both CTAs; compute/reducer warps arrive on the leader's barriers
 // remotely.  tau is folded into dK / dQ at their write-out.
@@ -50,34 +51,37 @@ constexpr uint32_t kHBox = 8192;   // [64 rows][64 d] bf16
 // dynamic smem map (bytes); the base is 1024-aligned (no static smem is used)
 constexpr uint32_t kOffK = 0;                     // own K, K-major: A of S^T = K Q^T
 constexpr uint32_t kOffV = kOffK + kTile;         // own V, K-major: A of dP^T = V dO^T
+constexpr uint32_t kStageA = 2 * kHBox;           // one [64 rows][128 d] K-major stage
+constexpr int kStagesA = 1;  // single-stage Q/dO row halves: 2 stages measured slower (TMA-reduce contention)
 constexpr uint32_t kOffQA = kOffV + kTile;        // Q rows [64r,+64), all d, K-major: B of S^T
-constexpr uint32_t kOffQB = kOffQA + 2 * kHBox;   // Q all rows, d cols [64r,+64), MN-major: B of dK
+constexpr uint32_t kOffQB = kOffQA + kStagesA * kStageA;  // Q all rows, d cols [64r,+64), MN-major: B of dK
 constexpr uint32_t kOffOA = kOffQB + kBox;        // dO rows half: B of dP^T
-constexpr uint32_t kOffOB = kOffOA + 2 * kHBox;   // dO cols half: B of dV
-constexpr uint32_t kOffDS = kOffOB + kBox;        // dS [128 keys][128 q] MN-major (two q halves): A of dQ
-constexpr uint32_t kOffDQ = kOffDS + kTile;       // 2 x [128 rows][32 fp32] reduce staging
-constexpr uint32_t kOffLSE = kOffDQ + 2 * 16384;  // 2 x 128 fp32 (LSE * log2 e)
+constexpr uint32_t kOffOB = kOffOA + kStagesA * kStageA;  // dO cols half: B of dV
+constexpr uint32_t kOffDS = kOffOB + kBox;        // dS [128 keys][128 q] (two q halves): A of dQ and dK
+constexpr int kDqBufs = 2;  // 4 buffers measured slower: the reduces queue ahead of Q/dO loads on the TMA unit
+constexpr uint32_t kOffDQ = kOffDS + kTile;       // kDqBufs x [128 rows][32 fp32] reduce staging
+constexpr uint32_t kOffLSE = kOffDQ + kDqBufs * 16384;  // 2 x 128 fp32 (LSE * log2 e)
 constexpr uint32_t kOffDelta = kOffLSE + 1024;    // 2 x 128 fp32
 constexpr uint32_t kOffBars = kOffDelta + 1024;
 constexpr uint32_t kSmemBytes = kOffBars + 256;
 static_assert(kSmemBytes <= 232448, "smem budget");
 
 constexpr uint32_t kIdescS = idesc_bf16(256, 128, 0, 0);  // pair, K-major x K-major
-constexpr uint32_t kIdescT = idesc_bf16(256, 128, 0, 1);  // pair, TMEM A x MN-major B
+constexpr uint32_t kIdescT = idesc_bf16(256, 128, 0, 1);  // pair, TMEM or K-major A x MN-major B
 constexpr uint32_t kIdescQ = idesc_bf16(128, 128, 1, 1);  // one CTA, MN-major x MN-major
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct Bars {
   uint64_t kv_full;                   // leader: K, V of both CTAs (tx)
-  uint64_t qa_full, qb_full;          // leader (tx of both CTAs)
-  uint64_t oa_full, ob_full;          // leader (tx of both CTAs)
-  uint64_t qa_empty, qb_empty;        // both (MMA commit multicast)
-  uint64_t oa_empty, ob_empty;        // both
+  uint64_t qa_full[2], qb_full;       // leader (tx of both CTAs)
+  uint64_t oa_full[2], ob_full;       // leader (tx of both CTAs)
+  uint64_t qa_empty[2], qb_empty;     // both (MMA commit multicast)
+  uint64_t oa_empty[2], ob_empty;     // both
   uint64_t lse_full[2], delta_full[2];    // local: producer lanes (32)
   uint64_t lse_empty[2], delta_empty[2];  // local: compute warps (8)
   uint64_t s_full, dp_full, dq_full;  // both (MMA commit multicast)
   uint64_t p_full, ds_full;           // leader: compute warps of both CTAs (16)
-  uint64_t ds_local;                  // local: compute warps (8), dS in this CTA's smem
+  uint64_t ds_local;                  // local: compute warps (8), dS in smem, dP read
   uint64_t dq_free;                   // leader: reducer warps of both CTAs (8)
   uint64_t dkdv_done;                 // both
   uint32_t tmem_base;
@@ -123,15 +127,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     if ((smem_u32(smem) & 1023u) != 0) __trap();  // SW128 atoms need 1024 B alignment
     mbar_init(&bars.kv_full, 1);
-    mbar_init(&bars.qa_full, 1);
     mbar_init(&bars.qb_full, 1);
-    mbar_init(&bars.oa_full, 1);
     mbar_init(&bars.ob_full, 1);
-    mbar_init(&bars.qa_empty, 1);
     mbar_init(&bars.qb_empty, 1);
-    mbar_init(&bars.oa_empty, 1);
     mbar_init(&bars.ob_empty, 1);
     for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars.qa_full[s], 1);
+      mbar_init(&bars.oa_full[s], 1);
+      mbar_init(&bars.qa_empty[s], 1);
+      mbar_init(&bars.oa_empty[s], 1);
       mbar_init(&bars.lse_full[s], 32);
       mbar_init(&bars.delta_full[s], 32);
       mbar_init(&bars.lse_empty[s], 8);
@@ -156,8 +160,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tS = tmem, tdV = tmem + 128, tdP = tmem + 256, tdK = tmem + 384;
   // leader-side barriers as shared::cluster addresses
   const uint32_t L_kv = mapa(smem_u32(&bars.kv_full), 0);
-  const uint32_t L_qa = mapa(smem_u32(&bars.qa_full), 0), L_qb = mapa(smem_u32(&bars.qb_full), 0);
-  const uint32_t L_oa = mapa(smem_u32(&bars.oa_full), 0), L_ob = mapa(smem_u32(&bars.ob_full), 0);
+  const uint32_t L_qb = mapa(smem_u32(&bars.qb_full), 0), L_ob = mapa(smem_u32(&bars.ob_full), 0);
   // debug trace of CTA (0,0): clock64 per pipeline event (SPPO_TRACE)
   unsigned long long* tr = (p.trace && blockIdx.x == 0 && blockIdx.y == 0) ? p.trace : nullptr;
 #define TR(slot, it)                                                              \
@@ -183,11 +186,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int m = 0; m < M; ++m) {
         const int s = m & 1;
         const int q0 = qtile(m) * BQ;
-        if (m > 0) mbar_wait(&bars.qa_empty, (m - 1) & 1);
+        const int sa = m % kStagesA, ua = m / kStagesA;  // stage and its use count
+        if (ua > 0) mbar_wait(&bars.qa_empty[sa], (ua - 1) & 1);
         if (lane == 0) {
-          if (leader) mbar_arrive_expect_tx(&bars.qa_full, 2 * 2 * kHBox);
-          tma_load_3d_pair(smem + kOffQA, mq64, L_qa, 0, head, q0 + 64 * (int)rank);
-          tma_load_3d_pair(smem + kOffQA + kHBox, mq64, L_qa, 64, head, q0 + 64 * (int)rank);
+          const uint32_t L_qa = mapa(smem_u32(&bars.qa_full[sa]), 0);
+          if (leader) mbar_arrive_expect_tx(&bars.qa_full[sa], 2 * kStageA);
+          tma_load_3d_pair(smem + kOffQA + sa * kStageA, mq64, L_qa, 0, head, q0 + 64 * (int)rank);
+          tma_load_3d_pair(smem + kOffQA + sa * kStageA + kHBox, mq64, L_qa, 64, head, q0 + 64 * (int)rank);
         }
         if (m >= 2) mbar_wait(&bars.lse_empty[s], ((m >> 1) - 1) & 1);
         float4 w;
@@ -208,11 +213,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int m = 0; m < M; ++m) {
         const int s = m & 1;
         const int q0 = qtile(m) * BQ;
-        if (m > 0) mbar_wait(&bars.oa_empty, (m - 1) & 1);
+        const int sa = m % kStagesA, ua = m / kStagesA;
+        if (ua > 0) mbar_wait(&bars.oa_empty[sa], (ua - 1) & 1);
         if (lane == 0) {
-          if (leader) mbar_arrive_expect_tx(&bars.oa_full, 2 * 2 * kHBox);
-          tma_load_3d_pair(smem + kOffOA, mdo64, L_oa, 0, head, q0 + 64 * (int)rank);
-          tma_load_3d_pair(smem + kOffOA + kHBox, mdo64, L_oa, 64, head, q0 + 64 * (int)rank);
+          const uint32_t L_oa = mapa(smem_u32(&bars.oa_full[sa]), 0);
+          if (leader) mbar_arrive_expect_tx(&bars.oa_full[sa], 2 * kStageA);
+          tma_load_3d_pair(smem + kOffOA + sa * kStageA, mdo64, L_oa, 0, head, q0 + 64 * (int)rank);
+          tma_load_3d_pair(smem + kOffOA + sa * kStageA + kHBox, mdo64, L_oa, 64, head, q0 + 64 * (int)rank);
         }
         if (m >= 2) mbar_wait(&bars.delta_empty[s], ((m >> 1) - 1) & 1);
         float4 w;
@@ -251,6 +258,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint64_t dQB_mn = sdesc_mnmajor(smem_u32(smem + kOffQB), kBox);
       const uint64_t dOB_mn = sdesc_mnmajor(smem_u32(smem + kOffOB), kBox);
       const uint64_t dDS_mn = sdesc_mnmajor(smem_u32(smem + kOffDS), kBox);
+      const uint64_t dDS_k = sdesc_kmajor(smem_u32(smem + kOffDS));
       const uint64_t dK_mn = sdesc_mnmajor(smem_u32(smem + kOffK), kBox);
       auto koff = [](int k) { return (uint64_t)(((k >> 2) * kBox + (k & 3) * 32) >> 4); };    // 128-row K-major
       auto koffh = [](int k) { return (uint64_t)(((k >> 2) * kHBox + (k & 3) * 32) >> 4); };  // 64-row K-major
@@ -263,8 +271,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       };
       if (!leader) {
         for (int m = 0; m < M; ++m) {
-          mbar_wait(&bars.ds_local, m & 1);  // dS(m) in this CTA's smem
-          mbar_wait(&bars.qb_empty, m & 1);  // pair dK(m) done: it no longer reads dS^T in tdP
+          mbar_wait(&bars.ds_local, m & 1);  // dS(m) in this CTA's smem, dP(m) read out of tdP
           tc_fence_after();
           mma_dq();
         }
@@ -282,20 +289,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mma2_ts_w(d, tA + (k >> 2) * 64 + (k & 3) * 8, B + moff(k), kIdescT, (acc || k > 0) ? 1u : 0u);
         };
         mbar_wait(&bars.kv_full, 0);
-        mbar_wait(&bars.qa_full, 0);
+        constexpr uint64_t kStageStep = kStageA >> 4;
+        mbar_wait(&bars.qa_full[0], 0);
         tc_fence_after();
         mma_kk(tS, dK_k, dQA_k);  // S^T(0) = K Q^T
         mma2_commit_w(&bars.s_full);
-        mma2_commit_w(&bars.qa_empty);
+        mma2_commit_w(&bars.qa_empty[0]);
         for (int m = 0; m < M; ++m) {
           TR(0, m);
-          mbar_wait(&bars.oa_full, m & 1);
+          mbar_wait(&bars.oa_full[m % kStagesA], (m / kStagesA) & 1);
           if (m > 0) mbar_wait(&bars.dq_free, (m - 1) & 1);  // both CTAs' reducers have read dQ(m-1)
           tc_fence_after();
           TR(1, m);
-          mma_kk(tdP, dV_k, dOA_k);  // dP^T = V dO^T
+          mma_kk(tdP, dV_k, dOA_k + (m % kStagesA) * kStageStep);  // dP^T = V dO^T
           mma2_commit_w(&bars.dp_full);
-          mma2_commit_w(&bars.oa_empty);
+          mma2_commit_w(&bars.oa_empty[m % kStagesA]);
           mbar_wait(&bars.p_full, m & 1);
           mbar_wait(&bars.ob_full, m & 1);
           tc_fence_after();
@@ -303,20 +311,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mma_tmemA(tdV, tS, dOB_mn, m > 0);  // dV += P^T dO
           mma2_commit_w(&bars.ob_empty);
           if (m + 1 < M) {
-            mbar_wait(&bars.qa_full, (m + 1) & 1);
+            const int n1 = m + 1;
+            mbar_wait(&bars.qa_full[n1 % kStagesA], (n1 / kStagesA) & 1);
             tc_fence_after();
             TR(3, m);
-            mma_kk(tS, dK_k, dQA_k);  // S^T(m+1): P(m) already consumed (in-order pipe)
+            mma_kk(tS, dK_k, dQA_k + (n1 % kStagesA) * kStageStep);  // S^T(m+1): P(m) consumed (in-order pipe)
             mma2_commit_w(&bars.s_full);
-            mma2_commit_w(&bars.qa_empty);
+            mma2_commit_w(&bars.qa_empty[n1 % kStagesA]);
           }
-          mbar_wait(&bars.ds_full, m & 1);  // implies this CTA's ds_local(m)
-          mbar_wait(&bars.qb_full, m & 1);
+          mbar_wait(&bars.ds_full, m & 1);  // both CTAs: dS(m) in smem (implies own ds_local(m))
           tc_fence_after();
           TR(4, m);
-          mma_tmemA(tdK, tdP, dQB_mn, m > 0);  // dK += dS^T Q
+          mma_dq();  // own dQ first: its readout overlaps the pair dK below
+          mbar_wait(&bars.qb_full, m & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < BQ / 16; ++k)  // dK += dS^T Q  (A = dS^T: rows = keys, K-major over q)
+            mma2_ss_w(tdK, dDS_k + koff(k), dQB_mn + moff(k), kIdescT, (m > 0 || k > 0) ? 1u : 0u);
           mma2_commit_w(&bars.qb_empty);
-          mma_dq();  // own dQ: after the pair dK in this SM's in-order tensor pipe
           TR(5, m);
         }
         mma2_commit_w(&bars.dkdv_done);
@@ -346,9 +358,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (threadIdx.x == 0) TR(13, m);
 #pragma unroll
       for (int pc = 0; pc < 4; ++pc, ++piece_ctr) {
-        const int buf = piece_ctr & 1;
+        const int buf = piece_ctr % kDqBufs;
         uint8_t* stg = smem + kOffDQ + buf * 16384;
-        if (threadIdx.x == 0) bulk_wait_read<1>();  // the reduce that last read `buf` is done
+        if (threadIdx.x == 0) bulk_wait_read<kDqBufs - 1>();  // the reduce that last read `buf` is done
         named_bar_sync(5, 128);
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch) {  // dQ = tau (dS K): tau applied here (dS is unscaled)
@@ -365,6 +377,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           bulk_commit();
         }
       }
+      if (threadIdx.x == 0) TR(14, m);
     }
     if (threadIdx.x == 0) bulk_wait<0>();
   } else {
@@ -456,13 +469,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           pk[c2] = pack_bf16(a0.x, a0.y);
           pk[c2 + 1] = pack_bf16(a1.x, a1.y);
         }
-        tmem_st16(tPg + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&pk[16 * h]));  // dS^T: A of dK += dS^T Q
 #pragma unroll
-        for (int ch = 4 * h; ch < 4 * h + 4; ++ch)  // dS as MN-major A of dQ = dS K: row = key, 64 q per half
+        for (int ch = 4 * h; ch < 4 * h + 4; ++ch)  // dS: row = key, 64 q per half (A of dQ and of dK)
           *reinterpret_cast<uint4*>(sDS + sw128(row, ch * 16)) =
               make_uint4(pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
       }
-      tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();

@@ -10,5 +10,5 @@ def med(a, b, nxt=False):
     v = [(rows[i + 1] if nxt else rows[i])[b] - rows[i][a] for i in range(len(rows) - 1) if rows[i][a] and rows[i][b]]
     return statistics.median(v) if v else None
 print("period", med(2, 2, True))
-for a, b in [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (6, 7), (7, 8), (8, 9), (1, 8), (9, 4), (12, 13), (5, 12)]:
+for a, b in [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (6, 7), (7, 8), (8, 9), (1, 8), (9, 4), (12, 13), (5, 12), (13, 14)]:
     print(f"{names[a]:>8} -> {names[b]:<8} {med(a, b)}")
