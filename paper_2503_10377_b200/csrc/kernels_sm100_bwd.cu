@@ -78,10 +78,10 @@ struct Bars {
   uint64_t qa_empty[2], qb_empty;     // both (MMA commit multicast)
   uint64_t oa_empty[2], ob_empty;     // both
   uint64_t lse_full[2], delta_full[2];    // local: producer lanes (32)
-  uint64_t lse_empty[2], delta_empty[2];  // local: compute warps (8)
+  uint64_t lse_empty[2], delta_empty[2];  // local: compute threads (256)
   uint64_t s_full, dp_full, dq_full;  // both (MMA commit multicast)
   uint64_t p_full, ds_full;           // leader: compute warps of both CTAs (16)
-  uint64_t ds_local;                  // local: compute warps (8), dS in smem, dP read
+  uint64_t ds_local;                  // peer only: compute threads (256), dS in smem, dP read
   uint64_t dq_free;                   // leader: reducer warps of both CTAs (8)
   uint64_t dkdv_done;                 // both
   uint32_t tmem_base;
@@ -138,15 +138,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&bars.oa_empty[s], 1);
       mbar_init(&bars.lse_full[s], 32);
       mbar_init(&bars.delta_full[s], 32);
-      mbar_init(&bars.lse_empty[s], 8);
-      mbar_init(&bars.delta_empty[s], 8);
+      mbar_init(&bars.lse_empty[s], 256);
+      mbar_init(&bars.delta_empty[s], 256);
     }
     mbar_init(&bars.s_full, 1);
     mbar_init(&bars.dp_full, 1);
     mbar_init(&bars.dq_full, 1);
     mbar_init(&bars.p_full, 16);
     mbar_init(&bars.ds_full, 16);
-    mbar_init(&bars.ds_local, 8);
+    mbar_init(&bars.ds_local, 256);
     mbar_init(&bars.dq_free, 8);
     mbar_init(&bars.dkdv_done, 1);
     fence_mbar_init();
@@ -206,6 +206,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) TR(15, m);
         mbar_arrive(&bars.lse_full[s]);
       }
+      for (int m = max(M - 2, 0); m < M; ++m) mbar_wait(&bars.lse_empty[m & 1], (m >> 1) & 1);
     } else if (warp == 15) {
       // ===================== TMA: dO rows half + Delta per tile =====================
       const CUtensorMap* mdo64 = tmap(a, a.do64_slot);
@@ -232,6 +233,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         *reinterpret_cast<float4*>(sDelta + s * 128 + lane * 4) = w;
         mbar_arrive(&bars.delta_full[s]);
       }
+      for (int m = max(M - 2, 0); m < M; ++m) mbar_wait(&bars.delta_empty[m & 1], (m >> 1) & 1);
     } else if (warp == 14) {
       // ===================== TMA: dO columns half, Q columns half per tile =====================
       const CUtensorMap* mq = tmap(a, a.q_slot);
@@ -438,11 +440,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       tmem_wait_st();
       tc_fence_before();
+      mbar_arrive(&bars.lse_empty[s]);  // every thread: its LSE reads are done
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_cluster(L_p_full);
-        mbar_arrive(&bars.lse_empty[s]);
-      }
+      if (lane == 0) mbar_arrive_cluster(L_p_full);
       if (lane == 0 && wq == 0 && g == 0) TR(7, m);
 
       // ---- dS = P (dP - Delta)   (tau is applied to dK / dQ at their write-out)
@@ -476,12 +476,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       fence_proxy_async_smem();
       tc_fence_before();
+      mbar_arrive(&bars.delta_empty[s]);  // every thread: its Delta reads are done
+      if (!leader) mbar_arrive(&bars.ds_local);  // the peer's own dQ MMA waits on this
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_cluster(L_ds_full);
-        mbar_arrive(&bars.ds_local);
-        mbar_arrive(&bars.delta_empty[s]);
-      }
+      if (lane == 0) mbar_arrive_cluster(L_ds_full);
       if (lane == 0 && wq == 0) TR(9 + 2 * g, m);
     }
     // ---- epilogue: dK_j, dV_j of this key tile (+= into the fp32 accumulators)
