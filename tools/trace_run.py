@@ -20,6 +20,8 @@ x = {t: make_tensor(t, S, range(h), 128, device="cuda") for t in ("q", "k", "v",
 eng = engine.ChunkedAttention(ctx, L)
 eng.step(x["q"], x["k"], x["v"], x["do"])
 ctx.sync()
+if "SPPO_TRACE" not in os.environ:  # plain step (e.g. under ncu)
+    sys.exit(0)
 rows = [list(map(int, l.split())) for l in open(os.environ["SPPO_TRACE"])]
 print(kind, "iters", len(rows))
 if kind == "bwd":
