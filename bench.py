@@ -18,6 +18,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -131,7 +132,12 @@ def cpu_oracle_sample(seconds_target=12.0):
     oracle.chunked_attention_bwd(xn["q"], xn["k"], xn["v"], o, lse, xn["do"], off)
     dt = time.perf_counter() - t0
     fl = 14 * 128 * (S_s * (S_s + 1) // 2)
-    return dict(value=fl / dt / 1e12, cores=int(cores), seconds=dt,
+    model = platform.processor()
+    try:
+        model = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+    except (OSError, StopIteration):
+        pass
+    return dict(value=fl / dt / 1e12, cores=int(cores), seconds=dt, cpu_model=model,
                 sample=f"oracle fp64 chunked fwd+bwd, 1 head x {S_s} tokens in {N_s} chunks of 8192 (C2 chunk length), "
                        f"{fl:.3e} FLOP in {dt:.1f}s")
 
@@ -270,24 +276,33 @@ def run_ours(args, cfg, ws, rank, local):
         eng.timing = False
 
         def time_offload(al):
+            """median step ms and its forward / backward phases (ms); al=None: resident"""
             res, moved = [], None
             for rep in range(1 + max(1, args.steps // 2)):
                 torch.cuda.synchronize()
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
+                e0, em, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                 e0.record(stream)
-                moved = eng.step_offload(x["q"], x["k"], x["v"], x["do"], al, stream)
+                if al is None:
+                    eng.step(x["q"], x["k"], x["v"], x["do"], stream, mark=em)
+                else:
+                    moved = eng.step_offload(x["q"], x["k"], x["v"], x["do"], al, stream, mark=em)
                 e1.record(stream)
                 torch.cuda.synchronize()
                 if rep > 0:
-                    res.append(e0.elapsed_time(e1))
-            return max_over_ranks(statistics.median(res), ws), moved
+                    res.append((e0.elapsed_time(e1), e0.elapsed_time(em), em.elapsed_time(e1)))
+            med = [max_over_ranks(statistics.median(r[j] for r in res), ws) for j in range(3)]
+            return med, moved
 
-        off_ms, moved = time_offload(alpha)
-        fix_ms, fix_moved = time_offload([1.0] * (N - 1) + [0.0])  # fixed full offload (P:250 baseline policy)
+        (res_ms, res_f, res_b), _ = time_offload(None)  # resident, same session, phase-split
+        (off_ms, off_f, off_b), moved = time_offload(alpha)
+        (fix_ms, _, _), fix_moved = time_offload([1.0] * (N - 1) + [0.0])  # fixed full offload (P:250 baseline)
         offload = {"policy": "type1-alpha (Q,O,LSE offloaded after fwd(i), prefetched depth 2 before bwd(i))",
                    "ms_per_step": round(off_ms, 3), "resident_ms_per_step": round(ms, 3),
                    "exposed_pct": round(100.0 * (off_ms - ms) / ms, 2),
+                   "exposed_split_pct": {"fwd": round(100.0 * (off_f - res_f) / res_ms, 2),
+                                         "bwd": round(100.0 * (off_b - res_b) / res_ms, 2),
+                                         "resident_ms_this_run": round(res_ms, 3),
+                                         "note": "phase times vs a resident step timed in the same loop"},
                    "d2h_bytes": moved["d2h"], "h2d_bytes": moved["h2d"],
                    "alpha": [round(a, 3) for a in alpha], "bw_d2h_gbs_assumed": bw / 1e9,
                    "fixed_alpha1": {"ms_per_step": round(fix_ms, 3), "exposed_pct": round(100.0 * (fix_ms - ms) / ms, 2),
@@ -335,7 +350,9 @@ def run_ours(args, cfg, ws, rank, local):
     if rank == 0 and ws == 1 and not args.no_cpu:
         c = cpu_oracle_sample()
         cpu = {"value": round(c["value"], 6), "unit": "TFLOP/s", "cores": c["cores"], "kind": "oracle",
-               "sample": c["sample"]}
+               "sample": c["sample"], "cpu_model": c["cpu_model"],
+               "full_oracle_hours_extrapolated": round(fl_total / (c["value"] * 1e12) / 3600, 1),
+               "more": "tools/oracle_timing.py -> profiles/r01/oracle_timing.json (C1 full, 1 thread)"}
 
     ctx.close()
     if rank != 0:

@@ -130,13 +130,16 @@ class ChunkedAttention:
             end.record(strm)
 
     # one step, all activations resident ---------------------------------------
-    def step(self, q, k, v, do, stream=None):
-        """Full forward + backward over all chunks (resident policy)."""
+    def step(self, q, k, v, do, stream=None, mark=None):
+        """Full forward + backward over all chunks (resident policy).  ``mark``
+        (a torch.cuda.Event) is recorded between the forward and backward phases."""
         N = self.L.num_chunks
         self.dk_acc.zero_()
         self.dv_acc.zero_()
         for i in range(N):
             self.forward_chunk(i, q, k, v, stream)
+        if mark is not None:
+            mark.record(stream or torch.cuda.current_stream())
         for i in range(N - 1, -1, -1):
             self.backward_chunk(i, q, k, v, do, stream)
         return dict(o=self.o, lse=self.lse, dq=self.dq, dk=self.dk, dv=self.dv)
@@ -157,7 +160,7 @@ class ChunkedAttention:
             self.ctx.host_free(ptr)
         self._host.clear()
 
-    def step_offload(self, q, k, v, do, alpha, stream=None, depth: int = 2, poison: bool = False):
+    def step_offload(self, q, k, v, do, alpha, stream=None, depth: int = 2, poison: bool = False, mark=None):
         """Forward + backward where Q_i, O_i and LSE_i leave the GPU after fwd(i)
         (alpha_i-prefix of each token-major buffer, LSE whole when alpha_i > 0)
         and come back before bwd(i).  With ``poison`` the device copies are
@@ -190,6 +193,8 @@ class ChunkedAttention:
                 for _, t, _, n, ev in parts:
                     strm.wait_event(ev)
                     t.reshape(-1).view(torch.uint8)[:n].fill_(0xFF)  # first n BYTES: NaN pattern in bf16/fp32
+        if mark is not None:
+            mark.record(strm)
         issued = set()
 
         def prefetch(i):
