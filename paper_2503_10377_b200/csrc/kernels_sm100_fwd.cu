@@ -36,7 +36,10 @@ constexpr uint32_t kHalf = kTileBytes / 2;       // one box: 128 rows x 64 cols
 constexpr int kSmemBytes = 6 * kTileBytes + 1024;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;        // log2 units
-constexpr int kEmuEvery = 4;                     // 1 of every kEmuEvery exp2 pairs on the FMA pipe
+#ifndef SPPO_EMU_EVERY
+#define SPPO_EMU_EVERY 4  // measured best among 2, 3, 4, 6 (tools/gpu_abn.sh)
+#endif
+constexpr int kEmuEvery = SPPO_EMU_EVERY;        // 1 of every kEmuEvery exp2 pairs on the FMA pipe
 
 constexpr uint32_t kIdescS = idesc_bf16(128, 128, 0, 0);   // Q (K-major) x K (K-major)
 constexpr uint32_t kIdescPV = idesc_bf16(128, 128, 0, 1);  // P (TMEM) x V (MN-major)
