@@ -155,6 +155,18 @@ sppo_status sppo_attn_bwd(sppo_ctx ctx, const sppo_layout* layout, int32_t chunk
                           const void* q, const sppo_kv_set* kv, const sppo_bwd_args* a,
                           int32_t flags, void* stream);
 
+/*
+ * sppo_finalize — a7 as a standalone call: dst(dtype) = src(fp32), n elements,
+ * RNE for SPPO_BF16, a copy for SPPO_FP32.  For gradient accumulators that were
+ * completed outside the descending chunk order (e.g. rotated around a ring of
+ * GPUs, context parallelism): sppo_attn_bwd writes the final dK_i / dV_i itself
+ * only when its window holds chunk i and it is the last contributor.
+ *   src : DEVICE fp32, 16-byte aligned;  dst : DEVICE dtype, 16-byte aligned
+ *   n   : multiple of 4 (SPPO_E_SHAPE otherwise)
+ * Enqueued on `stream`.
+ */
+sppo_status sppo_finalize(sppo_ctx ctx, const float* src, void* dst, size_t n, int32_t dtype, void* stream);
+
 /* ---- two-level activation management: pinned host arena + copies ------- */
 
 /* Pinned (page-locked) host memory (P:472 [§7]: "page-locked memory").    */

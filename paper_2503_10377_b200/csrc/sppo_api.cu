@@ -655,6 +655,18 @@ sppo_status sppo_causal_pairs(const int64_t* off, int32_t N, int64_t* pairs) {
   return SPPO_OK;
 }
 
+sppo_status sppo_finalize(sppo_ctx ctx, const float* src, void* dst, size_t n, int32_t dtype, void* stream) {
+  if (!ctx || !src || !dst) return fail(SPPO_E_ARG, "NULL argument");
+  if (dtype != SPPO_BF16 && dtype != SPPO_FP32) return fail(SPPO_E_ARG, "dtype = %d", dtype);
+  if (n % 4) return fail(SPPO_E_SHAPE, "n = %zu is not a multiple of 4", n);
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u)
+    return fail(SPPO_E_ALIGN, "src/dst must be 16-byte aligned");
+  SPPO_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaError_t e = launch_cast_f32(src, dst, n, dtype == SPPO_BF16, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "sppo_finalize");
+  return SPPO_OK;
+}
+
 sppo_status sppo_offload_alpha(const double* A, const double* m_threshold, int32_t N, double last, double* alpha) {
   if (!A || !m_threshold || !alpha) return fail(SPPO_E_ARG, "NULL argument");
   if (N < 1) return fail(SPPO_E_SHAPE, "N < 1");

@@ -27,7 +27,8 @@ STATUS = {0: "SPPO_OK", 1: "SPPO_E_ARG", 2: "SPPO_E_SHAPE", 3: "SPPO_E_ALIGN", 4
 # every symbol include/sppo.h declares
 EXPORTS = ("sppo_ctx_create", "sppo_ctx_destroy", "sppo_ctx_sync", "sppo_last_error", "sppo_version",
            "sppo_attn_fwd", "sppo_attn_bwd", "sppo_host_alloc", "sppo_host_free", "sppo_kv_offload",
-           "sppo_kv_prefetch", "sppo_partition_equal", "sppo_partition_balanced", "sppo_causal_pairs", "sppo_offload_alpha")
+           "sppo_kv_prefetch", "sppo_partition_equal", "sppo_partition_balanced", "sppo_causal_pairs", "sppo_offload_alpha",
+           "sppo_finalize")
 
 
 class SppoError(RuntimeError):
@@ -80,6 +81,7 @@ def _load():
         "sppo_causal_pairs": ([C.POINTER(C.c_int64), i32, C.POINTER(C.c_int64)], i32),
         "sppo_offload_alpha": ([C.POINTER(C.c_double), C.POINTER(C.c_double), i32, C.c_double,
                                 C.POINTER(C.c_double)], i32),
+        "sppo_finalize": ([vp, vp, vp, sz, i32, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -225,6 +227,10 @@ class Context:
                         _ptr(dq), _ptr(dk), _ptr(dv))
         _check(_lib.sppo_attn_bwd(self.h, C.byref(layout.c), chunk, _ptr(q), C.byref(kv), C.byref(args), flags,
                                   _stream(stream)))
+
+    def finalize(self, src, dst, dtype: int = SPPO_BF16, stream=None):
+        """a7: dst(dtype) = src(fp32) over src.numel() elements (sppo_finalize)."""
+        _check(_lib.sppo_finalize(self.h, _ptr(src), _ptr(dst), src.numel(), dtype, _stream(stream)))
 
     # -------------------------------------------------------------- host arena / copies
     def host_alloc(self, nbytes: int) -> int:
