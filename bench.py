@@ -386,6 +386,69 @@ def run_ours(args, cfg, ws, rank, local):
     return line
 
 
+# ------------------------------------------------------------------ context parallelism
+def run_cp(args, cfg, ws, rank, local):
+    """--parallel cp: the sequence sharded over the ranks (zigzag chunks), all heads
+    on every rank, K/V (and dK/dV accumulators) rotated around the ring
+    (paper_2503_10377_b200.cp).  value = whole-problem FLOPs / max-over-ranks time."""
+    from paper_2503_10377_b200 import cp, sppo
+    from synth import make_tensor
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    h, d, S, N = cfg["heads"], cfg["d"], cfg["S"], cfg["N"]
+    dtype = sppo.SPPO_BF16 if cfg["dtype"] == "bf16" else sppo.SPPO_FP32
+    tdt = torch.bfloat16 if dtype == sppo.SPPO_BF16 else torch.float32
+    ctx = sppo.Context(local)
+    offsets = sppo.partition_equal(S, N)
+    L = sppo.Layout(h, d, offsets, dtype=dtype)
+    own = cp.owned_chunks(N, ws, rank)
+    x = {}
+    for t in ("q", "k", "v", "do"):  # this rank's own tokens only (seeds per global head)
+        full = make_tensor(t, S, range(h), d, seed=0, dtype=tdt, device=dev)
+        x[t] = torch.cat([full[offsets[i]:offsets[i + 1]] for i in own]).contiguous()
+        del full
+    ra = cp.RingAttention(ctx, L, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ra.forward(x["q"], x["k"], x["v"], stream)
+        ra.backward(x["q"], x["k"], x["v"], x["do"], stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = ClockSampler(local)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    barrier(ws)
+    ms = max_over_ranks(t0.elapsed_time(t1) / args.steps, ws)
+    fl = flops_of(offsets, h, d)
+    peaks = load_peaks()
+    ctx.close()
+    if rank != 0:
+        return None
+    tflops = fl / (ms * 1e-3) / 1e12
+    return {"metric": METRIC, "value": round(tflops, 2), "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+            "config": {"workload": cfg["workload"], "heads": h, "head_dim": d, "seq_len": S, "chunks": N,
+                       "parallelism": f"context parallel: sequence zigzag-sharded over {ws} GPU(s), K/V ring "
+                                      f"(P2P), all heads per GPU",
+                       "l2": "inputs > 126 MB L2 (no flush needed)"},
+            "per_gpu_tflops": round(tflops / ws, 2),
+            "pct_bf16_peak": {"burst": round(100 * tflops / ws / peaks["burst"], 1), "source": peaks["source"]},
+            "tokens_per_s": round(S / (ms * 1e-3), 1), "clocks": clocks, "gpu_launches": None,
+            "note": "kernel roofline / e2e / offload / cpu_baseline: see the default (--parallel heads) line"}
+
+
 # ------------------------------------------------------------------ reference arm (the oracle)
 def run_reference(args, cfg, ws, rank):
     if rank != 0:
@@ -421,12 +484,19 @@ def main():
     ap.add_argument("--kv-window", type=int, default=4)
     ap.add_argument("--partition", default="equal", choices=["equal", "balanced"])
     ap.add_argument("--shard-of", type=int, default=1, help="1 GPU: run rank 0's heads of a G-GPU split")
+    ap.add_argument("--parallel", default="heads", choices=["heads", "cp"],
+                    help="multi-GPU split: heads (no collective in the step) or context-parallel ring")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: warmup < 3 violates the timing rules", file=sys.stderr)
     ws, rank, local = dist_setup()
     cfg = CONFIGS[args.config]
-    line = run_reference(args, cfg, ws, rank) if args.impl == "reference" else run_ours(args, cfg, ws, rank, local)
+    if args.impl == "reference":
+        line = run_reference(args, cfg, ws, rank)
+    elif args.parallel == "cp":
+        line = run_cp(args, cfg, ws, rank, local)
+    else:
+        line = run_ours(args, cfg, ws, rank, local)
     if line is not None:
         print(json.dumps(line), flush=True)
     if ws > 1:

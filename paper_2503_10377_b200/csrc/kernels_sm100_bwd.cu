@@ -58,6 +58,10 @@ constexpr uint32_t kOffQB = kOffQA + kStagesA * kStageA;  // Q all rows, d cols 
 constexpr uint32_t kOffOA = kOffQB + kBox;        // dO rows half: B of dP^T
 constexpr uint32_t kOffOB = kOffOA + kStagesA * kStageA;  // dO cols half: B of dV
 constexpr uint32_t kOffDS = kOffOB + kBox;        // dS [128 keys][128 q] (two q halves): A of dQ and dK
+#ifndef SPPO_DQ_RED_PIECES
+#define SPPO_DQ_RED_PIECES 0
+#endif
+constexpr int kDqRedPieces = SPPO_DQ_RED_PIECES;  // of the 4 dQ pieces, sent by red.global.add.v4.f32
 constexpr int kDqBufs = 2;  // 4 buffers measured slower: the reduces queue ahead of Q/dO loads on the TMA unit
 constexpr uint32_t kOffDQ = kOffDS + kTile;       // kDqBufs x [128 rows][32 fp32] reduce staging
 constexpr uint32_t kOffLSE = kOffDQ + kDqBufs * 16384;  // 2 x 128 fp32 (LSE * log2 e)
@@ -358,8 +362,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(L_dq_free);
       if (threadIdx.x == 0) TR(13, m);
+      // the last kDqRedPieces 32-column pieces go straight from registers as vector
+      // reductions (LSU path), in parallel with the TMA reduces of the others
 #pragma unroll
-      for (int pc = 0; pc < 4; ++pc, ++piece_ctr) {
+      for (int pc = 4 - kDqRedPieces; pc < 4; ++pc) {
+        if (q0 + row < p.q_len) {
+          float* dst = p.dq_acc + ((size_t)(q0 + row) * p.heads + head) * HD + pc * 32;
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * c4),
+                         "f"(__uint_as_float(v[pc * 32 + 4 * c4 + 0]) * tau),
+                         "f"(__uint_as_float(v[pc * 32 + 4 * c4 + 1]) * tau),
+                         "f"(__uint_as_float(v[pc * 32 + 4 * c4 + 2]) * tau),
+                         "f"(__uint_as_float(v[pc * 32 + 4 * c4 + 3]) * tau)
+                         : "memory");
+        }
+      }
+#pragma unroll
+      for (int pc = 0; pc < 4 - kDqRedPieces; ++pc, ++piece_ctr) {
         const int buf = piece_ctr % kDqBufs;
         uint8_t* stg = smem + kOffDQ + buf * 16384;
         if (threadIdx.x == 0) bulk_wait_read<kDqBufs - 1>();  // the reduce that last read `buf` is done

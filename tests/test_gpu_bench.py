@@ -1,0 +1,51 @@
+"""bench.py's JSON contract on the GPU (C1, the small fp32 config): the default
+head-sharded line with every required key, the context-parallel ring mode
+(--parallel cp) on one rank and on two ranks sharing the one GPU (gloo)."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REQUIRED = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+            "vs_baseline", "dtype", "data", "config", "clocks")
+
+
+def _run(cmd, env=None):
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env={**os.environ, **(env or {})})
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_bench_default_line_c1():
+    d = _run([sys.executable, "bench.py", "--config", "C1", "--steps", "3", "--warmup", "3", "--no-cpu"])
+    for k in REQUIRED + ("roofline", "e2e", "gpu_launches", "offload"):
+        assert k in d, k
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["dtype"] == "fp32"
+    assert d["roofline"]["frac"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+
+
+def test_bench_context_parallel_one_rank_c1():
+    d = _run([sys.executable, "bench.py", "--config", "C1", "--parallel", "cp", "--steps", "3", "--warmup", "3"])
+    for k in REQUIRED:
+        assert k in d, k
+    assert d["value"] > 0 and "context parallel" in d["config"]["parallelism"]
+
+
+def test_bench_context_parallel_two_ranks_one_gpu_c1():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    d = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+              "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--config", "C1",
+              "--parallel", "cp", "--steps", "3", "--warmup", "3"],
+             env={"SPPO_BENCH_DEVICE": "0", "SPPO_DIST_BACKEND": "gloo"})
+    assert d["n_gpus"] == 2 and d["value"] > 0
