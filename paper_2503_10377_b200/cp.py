@@ -80,6 +80,9 @@ class Ring:
         import torch.distributed as dist
         self.dist = dist
         self.group = group
+        if not dist.is_initialized():  # a ring of one (single process)
+            self.G, self.g, self.nccl = 1, 0, False
+            return
         self.G = dist.get_world_size(group)
         self.g = dist.get_rank(group)
         self.nccl = dist.get_backend(group) == "nccl"
@@ -88,6 +91,10 @@ class Ring:
         """Start sending `send` to g+1 and receiving into `recv` from g-1; returns a
         handle whose wait() completes the exchange (on the current stream for NCCL)."""
         dist = self.dist
+        if self.G == 1:  # the neighbour is this rank
+            for a, b in zip(send, recv):
+                b.copy_(a)
+            return _Handle([], None)
         nxt = (self.g + 1) % self.G
         prv = (self.g - 1) % self.G
         if self.nccl:

@@ -29,7 +29,7 @@ def test_bench_default_line_c1():
     for k in REQUIRED + ("roofline", "e2e", "gpu_launches", "offload"):
         assert k in d, k
     assert d["value"] > 0 and d["n_gpus"] == 1 and d["dtype"] == "fp32"
-    assert d["roofline"]["frac"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert d["roofline"]["achieved"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
 
 
 def test_bench_context_parallel_one_rank_c1():
