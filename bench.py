@@ -313,6 +313,26 @@ def run_ours(args, cfg, ws, rank, local):
 
     # ---- KV streaming policy (hot prefix resident, colder chunks streamed from host)
     kvs = None
+    budget = None
+    if args.device_budget > 0:
+        # SURVEY §8(a) note / reading L10: the largest hot prefix P whose resident bytes fit
+        # the budget; everything but K/V of chunks >= P stays resident, plus a 2-slot ring
+        # of W-chunk windows for the streamed K/V
+        el = eng.elem
+        tok = h * d
+        non_kv = S * tok * (6 * el + 2 * 4) + S * h * 4 * 2 + max(L.chunk_len(i) for i in range(N)) * tok * 8
+        ring = 2 * args.kv_window * max(L.chunk_len(i) for i in range(N)) * tok * 2 * el
+        kv_of = [L.chunk_len(i) * tok * 2 * el for i in range(N)]
+        room = args.device_budget * 1e9 - non_kv - ring
+        P = 0
+        while P < N and sum(kv_of[:P + 1]) <= room:
+            P += 1
+        if room < 0:
+            raise SystemExit(f"--device-budget {args.device_budget} GB is below the non-KV working set")
+        args.kv_hot = P
+        budget = {"device_budget_gb": args.device_budget, "hot_prefix_chosen": P,
+                  "resident_gb": round((non_kv + ring + sum(kv_of[:P])) / 1e9, 2),
+                  "all_resident_gb": round((non_kv + sum(kv_of)) / 1e9, 2)}
     if args.kv_hot >= 0:
         res = []
         st = None
@@ -332,7 +352,8 @@ def run_ours(args, cfg, ws, rank, local):
                          f"{args.kv_window} (2-slot ring) for every later fwd/bwd; Type-1 resident",
                "ms_per_step": round(kv_ms, 3), "resident_ms_per_step": round(ms, 3),
                "exposed_pct": round(100.0 * (kv_ms - ms) / ms, 2), "h2d_bytes": st["h2d"], "d2h_bytes": st["d2h"],
-               "h2d_gbs_achieved": round(st["h2d"] / (kv_ms * 1e-3) / 1e9, 1), "windows": st["windows"]}
+               "h2d_gbs_achieved": round(st["h2d"] / (kv_ms * 1e-3) / 1e9, 1), "windows": st["windows"],
+               "budget": budget}
         eng.free_host()
 
     # ---- final gather of O over NCCL (multi-GPU only, not timed in value)
@@ -482,6 +503,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--kv-hot", type=int, default=-1, help="also time KV streaming with this hot prefix (-1: skip)")
     ap.add_argument("--kv-window", type=int, default=4)
+    ap.add_argument("--device-budget", type=float, default=0.0,
+                    help="GB of device memory for the step: picks the KV hot prefix that fits (0: off)")
     ap.add_argument("--partition", default="equal", choices=["equal", "balanced"])
     ap.add_argument("--shard-of", type=int, default=1, help="1 GPU: run rank 0's heads of a G-GPU split")
     ap.add_argument("--parallel", default="heads", choices=["heads", "cp"],

@@ -49,3 +49,11 @@ def test_bench_context_parallel_two_ranks_one_gpu_c1():
               "--parallel", "cp", "--steps", "3", "--warmup", "3"],
              env={"SPPO_BENCH_DEVICE": "0", "SPPO_DIST_BACKEND": "gloo"})
     assert d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_bench_device_budget_picks_hot_prefix_c1():
+    """--device-budget: the largest KV hot prefix that fits is chosen and timed (reading L10)."""
+    d = _run([sys.executable, "bench.py", "--config", "C1", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e",
+              "--no-offload", "--device-budget", "0.0027", "--kv-window", "1"])
+    b = d["kv_stream"]["budget"]
+    assert 0 <= b["hot_prefix_chosen"] < 4 and b["resident_gb"] <= 0.0027 < b["all_resident_gb"]
