@@ -202,15 +202,20 @@ def run_ours(args, cfg, ws, rank, local):
         eng.step(x["q"], x["k"], x["v"], x["do"], stream)
     torch.cuda.synchronize()
     eng.events = {"fwd": [], "bwd": []}
+    eng.timing = False  # per-call events are not used for the timed steps (phase marks are)
+    phase = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     eng.launches = 0
     barrier(ws)
     torch.cuda.synchronize()
     clk = ClockSampler(local)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     t0.record(stream)
-    for _ in range(args.steps):
-        eng.step(x["q"], x["k"], x["v"], x["do"], stream)
+    for st in range(args.steps):
+        marks[st].record(stream)  # step start; eng.step records the fwd/bwd boundary in phase[st]
+        eng.step(x["q"], x["k"], x["v"], x["do"], stream, mark=phase[st])
+    marks[args.steps].record(stream)
     t1.record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
@@ -218,8 +223,10 @@ def run_ours(args, cfg, ws, rank, local):
     ms_local = t0.elapsed_time(t1) / args.steps
     ms = max_over_ranks(ms_local, ws)
     launches = eng.launches // args.steps
-    fwd_ms = eng.kernel_ms("fwd") / args.steps
-    bwd_ms = eng.kernel_ms("bwd") / args.steps
+    # phase times: forward = step start -> boundary (the two forward streams overlap, so
+    # per-call events would double count), backward = boundary -> next step start
+    fwd_ms = sum(marks[st].elapsed_time(phase[st]) for st in range(args.steps)) / args.steps
+    bwd_ms = sum(phase[st].elapsed_time(marks[st + 1]) for st in range(args.steps)) / args.steps
 
     fl_dev = flops_of(offsets, h, d)
     fl_total = flops_of(offsets, cfg["heads"] if args.shard_of == 1 else len(heads), d)
@@ -267,8 +274,10 @@ def run_ours(args, cfg, ws, rank, local):
     if not args.no_offload:
         bw = 56e9  # pinned D2H GB/s measured on this pool (tools/box_probe.py, gpurun_out/box_probe.json)
         eng.events = {"fwd": [], "bwd": []}
+        eng.timing, eng.fwd_streams = True, 1  # per-chunk forward times, one stream
         eng.step(x["q"], x["k"], x["v"], x["do"], stream)
         torch.cuda.synchronize()
+        eng.fwd_streams = 2
         t_fwd = [a.elapsed_time(b) * 1e-3 for a, b in eng.events["fwd"]]
         A = [eng.type1_bytes(i) for i in range(N)]
         thr = [bw * (t_fwd[i + 1] if i + 1 < N else 0.0) for i in range(N)]
@@ -331,8 +340,8 @@ def run_ours(args, cfg, ws, rank, local):
             raise SystemExit(f"--device-budget {args.device_budget} GB is below the non-KV working set")
         args.kv_hot = P
         budget = {"device_budget_gb": args.device_budget, "hot_prefix_chosen": P,
-                  "resident_gb": round((non_kv + ring + sum(kv_of[:P])) / 1e9, 2),
-                  "all_resident_gb": round((non_kv + sum(kv_of)) / 1e9, 2)}
+                  "resident_bytes": int(non_kv + ring + sum(kv_of[:P])),
+                  "all_resident_bytes": int(non_kv + sum(kv_of))}
     if args.kv_hot >= 0:
         res = []
         st = None

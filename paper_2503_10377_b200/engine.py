@@ -34,8 +34,13 @@ DTYPES = {sppo.SPPO_BF16: torch.bfloat16, sppo.SPPO_FP32: torch.float32}
 
 class ChunkedAttention:
     def __init__(self, ctx: sppo.Context, layout: sppo.Layout, device="cuda", window: int | None = None,
-                 timing: bool = False):
+                 timing: bool = False, fwd_streams: int = 2):
         self.ctx, self.L = ctx, layout
+        # resident step(): forward chunks are independent (chunk i reads only inputs), so
+        # consecutive forward launches alternate between two streams and the next one
+        # fills the SMs the previous one's last wave leaves idle
+        self.fwd_streams = fwd_streams
+        self._side = None
         self.device = torch.device(device)
         self.window = window if window else 10**9
         self.timing = timing
@@ -134,12 +139,25 @@ class ChunkedAttention:
         """Full forward + backward over all chunks (resident policy).  ``mark``
         (a torch.cuda.Event) is recorded between the forward and backward phases."""
         N = self.L.num_chunks
+        strm = stream or torch.cuda.current_stream()
         self.dk_acc.zero_()
         self.dv_acc.zero_()
+        # two forward streams only without split windows (those share the carry scratch)
+        two = self.fwd_streams > 1 and N > 1 and self.window >= N
+        if two:
+            if self._side is None:
+                self._side = torch.cuda.Stream(device=self.device)
+            fork = torch.cuda.Event()
+            fork.record(strm)
+            self._side.wait_event(fork)
         for i in range(N):
-            self.forward_chunk(i, q, k, v, stream)
+            self.forward_chunk(i, q, k, v, self._side if (two and i % 2) else strm)
+        if two:
+            join = torch.cuda.Event()
+            join.record(self._side)
+            strm.wait_event(join)
         if mark is not None:
-            mark.record(stream or torch.cuda.current_stream())
+            mark.record(strm)
         for i in range(N - 1, -1, -1):
             self.backward_chunk(i, q, k, v, do, stream)
         return dict(o=self.o, lse=self.lse, dq=self.dq, dk=self.dk, dv=self.dv)

@@ -56,4 +56,4 @@ def test_bench_device_budget_picks_hot_prefix_c1():
     d = _run([sys.executable, "bench.py", "--config", "C1", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e",
               "--no-offload", "--device-budget", "0.0027", "--kv-window", "1"])
     b = d["kv_stream"]["budget"]
-    assert 0 <= b["hot_prefix_chosen"] < 4 and b["resident_gb"] <= 0.0027 < b["all_resident_gb"]
+    assert 0 <= b["hot_prefix_chosen"] < 4 and b["resident_bytes"] <= 0.0027e9 < b["all_resident_bytes"]
