@@ -195,7 +195,7 @@ def run_ours(args, cfg, ws, rank, local):
     offsets = sppo.partition_balanced(S, N) if args.partition == "balanced" else sppo.partition_equal(S, N)
     L = sppo.Layout(h, d, offsets, dtype=dtype)
     x = {t: make_tensor(t, S, heads, d, seed=0, dtype=tdt, device=dev) for t in ("q", "k", "v", "do")}
-    eng = engine.ChunkedAttention(ctx, L, device=dev, timing=True)
+    eng = engine.ChunkedAttention(ctx, L, device=dev, timing=True, fwd_streams=args.fwd_streams)
     stream = torch.cuda.current_stream()
 
     for _ in range(args.warmup):
@@ -274,10 +274,11 @@ def run_ours(args, cfg, ws, rank, local):
     if not args.no_offload:
         bw = 56e9  # pinned D2H GB/s measured on this pool (tools/box_probe.py, gpurun_out/box_probe.json)
         eng.events = {"fwd": [], "bwd": []}
+        fs_default = eng.fwd_streams
         eng.timing, eng.fwd_streams = True, 1  # per-chunk forward times, one stream
         eng.step(x["q"], x["k"], x["v"], x["do"], stream)
         torch.cuda.synchronize()
-        eng.fwd_streams = 2
+        eng.fwd_streams = fs_default
         t_fwd = [a.elapsed_time(b) * 1e-3 for a, b in eng.events["fwd"]]
         A = [eng.type1_bytes(i) for i in range(N)]
         thr = [bw * (t_fwd[i + 1] if i + 1 < N else 0.0) for i in range(N)]
@@ -512,6 +513,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--kv-hot", type=int, default=-1, help="also time KV streaming with this hot prefix (-1: skip)")
     ap.add_argument("--kv-window", type=int, default=4)
+    ap.add_argument("--fwd-streams", type=int, default=None, choices=[1, 2],
+                    help="resident step: forward launches alternate over this many streams (default: by launch size)")
     ap.add_argument("--device-budget", type=float, default=0.0,
                     help="GB of device memory for the step: picks the KV hot prefix that fits (0: off)")
     ap.add_argument("--partition", default="equal", choices=["equal", "balanced"])

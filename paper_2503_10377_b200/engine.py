@@ -34,11 +34,20 @@ DTYPES = {sppo.SPPO_BF16: torch.bfloat16, sppo.SPPO_FP32: torch.float32}
 
 class ChunkedAttention:
     def __init__(self, ctx: sppo.Context, layout: sppo.Layout, device="cuda", window: int | None = None,
-                 timing: bool = False, fwd_streams: int = 2):
+                 timing: bool = False, fwd_streams: int | None = None):
         self.ctx, self.L = ctx, layout
         # resident step(): forward chunks are independent (chunk i reads only inputs), so
-        # consecutive forward launches alternate between two streams and the next one
-        # fills the SMs the previous one's last wave leaves idle
+        # consecutive forward launches may alternate between two streams and the next one
+        # fills the SMs the previous one's last wave leaves idle.  Measured: worth it
+        # when a launch is a few waves (C2 per-GPU shares at 2-8 GPUs: +5 %), harmful when
+        # it is many (C3, 14 waves: two kernels sweeping different K/V positions, -11 %
+        # forward).  Default: two streams below 8 waves of CTAs per launch.
+        if fwd_streams is None:
+            smax = max(layout.chunk_len(i) for i in range(layout.num_chunks))
+            ctas = -(-smax // 256) * layout.heads  # fwd_kernel: 2 Q tiles of 128 rows per CTA
+            sms = torch.cuda.get_device_properties(torch.device(device)).multi_processor_count \
+                if torch.cuda.is_available() else 148
+            fwd_streams = 2 if ctas < 8 * sms else 1
         self.fwd_streams = fwd_streams
         self._side = None
         self.device = torch.device(device)
