@@ -74,3 +74,25 @@ def test_ring_two_ranks_matches_oracle(tmp_path, S, h, N):
         for key in ("dq", "dk", "dv"):
             np.testing.assert_allclose(d[key], ref[key][rows], **G_TOL, err_msg=f"rank {r} {key}")
     assert sorted(covered) == list(range(S))
+
+
+def test_finalize_cast_and_errors():
+    """sppo_finalize (a7): RNE fp32 -> bf16 cast / fp32 copy; n % 4 and alignment checked."""
+    from paper_2503_10377_b200 import sppo
+    ctx = sppo.Context(0)
+    src = torch.randn(4096, device="cuda") * 3
+    dst = torch.empty(4096, dtype=torch.bfloat16, device="cuda")
+    ctx.finalize(src, dst, sppo.SPPO_BF16)
+    torch.cuda.synchronize()
+    assert torch.equal(dst, src.to(torch.bfloat16))
+    d32 = torch.empty(4096, device="cuda")
+    ctx.finalize(src, d32, sppo.SPPO_FP32)
+    torch.cuda.synchronize()
+    assert torch.equal(d32, src)
+    with pytest.raises(sppo.SppoError) as e:
+        ctx.finalize(src[:6], dst[:6], sppo.SPPO_BF16)
+    assert e.value.name == "SPPO_E_SHAPE"
+    with pytest.raises(sppo.SppoError) as e:
+        ctx.finalize(src[1:5], dst[:4], sppo.SPPO_BF16)
+    assert e.value.name == "SPPO_E_ALIGN"
+    ctx.close()
