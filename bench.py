@@ -10,6 +10,13 @@ heads are sharded over the ranks (Ulysses-style head parallelism without the
 all-to-all); no collective inside the step; one NCCL all-gather
 of O after timing (not timed).  Rank 0 prints one JSON line.
 
+Besides the resident step the line carries: the end-to-end step from/to pinned
+host memory (e2e), the Type-1 alpha offload policy (exposed %, split by phase),
+optionally KV streaming (--kv-hot / --device-budget), the bwd kernel's roofline
+object and the oracle's CPU baseline.  Other modes: --parallel cp (sequence
+ring, paper_2503_10377_b200/cp.py), --shard-of G (rank 0's share of a G-GPU
+head split on one GPU), --partition balanced, --impl reference (the oracle).
+
 FLOP convention: 4d per causal pair forward, 10d backward.
 """
 
