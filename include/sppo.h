@@ -208,6 +208,12 @@ enum {
 sppo_status sppo_kv_prefetch(sppo_ctx ctx, int32_t chunk, const void* host, void* dev,
                              size_t bytes, void* consumer, void* done, int32_t flags);
 
+/* The ctx's copy streams (cudaStream_t) that sppo_kv_offload (D2H) and
+ * sppo_kv_prefetch (H2D) enqueue on, for callers that order or time work
+ * against them (e.g. events recorded around copies for an overlap timeline).
+ * The ctx keeps ownership; either output may be NULL. */
+sppo_status sppo_ctx_streams(sppo_ctx ctx, void** d2h, void** h2d);
+
 /* ---- host-side plan helpers ----------------------- */
 
 /* Equal partition: N+1 offsets, first S mod N chunks longer. */

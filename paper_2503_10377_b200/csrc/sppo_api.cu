@@ -574,6 +574,13 @@ sppo_status sppo_kv_prefetch(sppo_ctx ctx, int32_t chunk, const void* host, void
   return SPPO_OK;
 }
 
+sppo_status sppo_ctx_streams(sppo_ctx ctx, void** d2h, void** h2d) {
+  if (!ctx) return fail(SPPO_E_ARG, "ctx is NULL");
+  if (d2h) *d2h = ctx->d2h;
+  if (h2d) *h2d = ctx->h2d;
+  return SPPO_OK;
+}
+
 // ---------------------------------------------------------------- plan helpers
 sppo_status sppo_partition_equal(int64_t S, int32_t N, int64_t* out) {
   if (!out) return fail(SPPO_E_ARG, "out is NULL");

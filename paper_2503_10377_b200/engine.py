@@ -50,6 +50,10 @@ class ChunkedAttention:
             fwd_streams = 2 if ctas < 8 * sms else 1
         self.fwd_streams = fwd_streams
         self._side = None
+        # instrumentation (tools/offload_timeline.py): when a list, every compute call
+        # and every copy appends {kind, chunk, bytes, events}; see _tl_begin/_tl_end
+        self.timeline = None
+        self._copy_streams = None
         self.device = torch.device(device)
         self.window = window if window else 10**9
         self.timing = timing
@@ -99,6 +103,34 @@ class ChunkedAttention:
         self.events[kind].append((e0, e1))
         return e1
 
+    def _tl_begin(self, kind, i, stream, nbytes=0, copy=None):
+        """copy=None: a compute call on `stream` (start event).  copy='d2h'/'h2d': an
+        event on that ctx copy stream before the call plus one on `stream` (the
+        producer / consumer): the copy starts at the later of the two."""
+        if self.timeline is None:
+            return None
+        ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        rec = {"kind": kind, "chunk": i, "bytes": nbytes}
+        if copy is None:
+            rec["e0"] = ev()
+            rec["e0"].record(stream)
+        else:
+            if self._copy_streams is None:
+                d2h, h2d = self.ctx.copy_streams()
+                self._copy_streams = {"d2h": torch.cuda.ExternalStream(d2h), "h2d": torch.cuda.ExternalStream(h2d)}
+            rec["cs"] = self._copy_streams[copy]
+            rec["eb"], rec["ep"] = ev(), ev()
+            rec["eb"].record(rec["cs"])
+            rec["ep"].record(stream)
+        return rec
+
+    def _tl_end(self, rec, stream=None):
+        if rec is None:
+            return
+        rec["e1"] = torch.cuda.Event(enable_timing=True)
+        rec["e1"].record(rec.get("cs", stream))
+        self.timeline.append(rec)
+
     def kernel_ms(self, kind):
         """Sum of CUDA-event durations of the recorded calls (after a sync)."""
         return sum(a.elapsed_time(b) for a, b in self.events[kind])
@@ -112,6 +144,7 @@ class ChunkedAttention:
         state = (self.o_acc[:s], self.m[:s * h], self.l[:s * h])
         strm = stream or torch.cuda.current_stream()
         end = self._ev("fwd", strm)
+        tl = self._tl_begin("fwd", i, strm)
         for n, ids in enumerate(wins):
             flags = (sppo.SPPO_FIRST if n == 0 else 0) | (sppo.SPPO_LAST if n == len(wins) - 1 else 0)
             self.ctx.attn_fwd(L, i, self.rows(q, i), ids, [self.rows(k, j) for j in ids],
@@ -119,6 +152,7 @@ class ChunkedAttention:
                               state=None if len(wins) == 1 else state,
                               o=self.rows(self.o, i), lse=self.lse_view(i), stream=strm)
             self.launches += 1
+        self._tl_end(tl, strm)
         if end is not None:
             end.record(strm)
 
@@ -129,6 +163,7 @@ class ChunkedAttention:
         wins = self.windows(i)
         strm = stream or torch.cuda.current_stream()
         end = self._ev("bwd", strm)
+        tl = self._tl_begin("bwd", i, strm)
         for n, ids in enumerate(wins):
             flags = (sppo.SPPO_FIRST if n == 0 else 0) | (sppo.SPPO_LAST if n == len(wins) - 1 else 0)
             has_i = i in ids
@@ -140,6 +175,7 @@ class ChunkedAttention:
                               dv=self.rows(self.dv, i) if has_i else None, flags=flags, stream=strm)
             # main kernel + Delta preprocess on FIRST + dQ cast on LAST
             self.launches += 1 + (flags & sppo.SPPO_FIRST != 0) + (flags & sppo.SPPO_LAST != 0)
+        self._tl_end(tl, strm)
         if end is not None:
             end.record(strm)
 
@@ -211,8 +247,12 @@ class ChunkedAttention:
                 nb = t.numel() * t.element_size()
                 host = self._host_buf((name, i), nb)
                 ev = torch.cuda.Event()
+                tl = self._tl_begin("d2h", i, strm, copy="d2h")
                 n = self.ctx.kv_offload(i, t, host, nb, alpha=(a if name != "lse" else 1.0), producer=strm,
                                         done=ev)
+                if tl is not None:
+                    tl["bytes"] = n
+                self._tl_end(tl)
                 moved["d2h"] += n
                 parts.append((name, t, host, n, ev))
             plan[i] = parts
@@ -233,8 +273,10 @@ class ChunkedAttention:
                 # bytes must have reached the host first (D2H of the offload)
                 strm.wait_event(ev)
                 pe = torch.cuda.Event()
+                tl = self._tl_begin("h2d", i, strm, n, copy="h2d")
                 self.ctx.kv_prefetch(i, host, t, n, consumer=strm, done=pe,
                                      flags=sppo.SPPO_COPY_DEFER_WAIT)
+                self._tl_end(tl)
                 moved["h2d"] += n
                 evs.append(pe)
             done[i] = evs

@@ -28,7 +28,7 @@ STATUS = {0: "SPPO_OK", 1: "SPPO_E_ARG", 2: "SPPO_E_SHAPE", 3: "SPPO_E_ALIGN", 4
 EXPORTS = ("sppo_ctx_create", "sppo_ctx_destroy", "sppo_ctx_sync", "sppo_last_error", "sppo_version",
            "sppo_attn_fwd", "sppo_attn_bwd", "sppo_host_alloc", "sppo_host_free", "sppo_kv_offload",
            "sppo_kv_prefetch", "sppo_partition_equal", "sppo_partition_balanced", "sppo_causal_pairs", "sppo_offload_alpha",
-           "sppo_finalize")
+           "sppo_finalize", "sppo_ctx_streams")
 
 
 class SppoError(RuntimeError):
@@ -82,6 +82,7 @@ def _load():
         "sppo_offload_alpha": ([C.POINTER(C.c_double), C.POINTER(C.c_double), i32, C.c_double,
                                 C.POINTER(C.c_double)], i32),
         "sppo_finalize": ([vp, vp, vp, sz, i32, vp], i32),
+        "sppo_ctx_streams": ([vp, C.POINTER(vp), C.POINTER(vp)], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -207,6 +208,12 @@ class Context:
 
     def sync(self):
         _check(_lib.sppo_ctx_sync(self.h))
+
+    def copy_streams(self):
+        """(d2h, h2d) cudaStream_t handles of the ctx (sppo_ctx_streams)."""
+        a, b = C.c_void_p(), C.c_void_p()
+        _check(_lib.sppo_ctx_streams(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     # -------------------------------------------------------------- attention
     def attn_fwd(self, layout: Layout, chunk: int, q, kv_ids, ks, vs, flags=SPPO_FIRST | SPPO_LAST, state=None,
