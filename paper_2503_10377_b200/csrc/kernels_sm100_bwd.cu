@@ -62,7 +62,11 @@ constexpr uint32_t kOffDS = kOffOB + kBox;        // dS [128 keys][128 q] (two q
 #define SPPO_DQ_RED_PIECES 0  // measured: 1 piece -> bwd 841, 2 -> 775 vs 1017 TF/s (L2/LSU bound)
 #endif
 constexpr int kDqRedPieces = SPPO_DQ_RED_PIECES;  // of the 4 dQ pieces, sent by red.global.add.v4.f32
-constexpr int kDqBufs = 2;  // 4 buffers measured slower: the reduces queue ahead of Q/dO loads on the TMA unit
+constexpr int kDqBufs = 2;
+#ifndef SPPO_EPI_RED
+#define SPPO_EPI_RED 1  // measured: bwd +3 % at C2, +9 % at 2K chunks vs load-add-store
+#endif
+constexpr bool kEpiRed = SPPO_EPI_RED;  // dK/dV accumulator epilogue: red.global.add (1) or load-add-store (0)  // 4 buffers measured slower: the reduces queue ahead of Q/dO loads on the TMA unit
 constexpr uint32_t kOffDQ = kOffDS + kTile;       // kDqBufs x [128 rows][32 fp32] reduce staging
 constexpr uint32_t kOffLSE = kOffDQ + kDqBufs * 16384;  // 2 x 128 fp32 (LSE * log2 e)
 constexpr uint32_t kOffDelta = kOffLSE + 1024;    // 2 x 128 fp32
@@ -522,8 +526,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int q4 = 0; q4 < 8; ++q4) {
             float4* ap = reinterpret_cast<float4*>(acc + half * 32 + q4 * 4);
-            float4 o = *ap;
             const float f = which == 0 ? 1.f : tau;  // dK = tau dS^T Q
+            if (kEpiRed && !final_out) {  // += as a fire-and-forget vector reduction (L2 does the RMW)
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(ap),
+                           "f"(__uint_as_float(v[q4 * 4 + 0]) * f), "f"(__uint_as_float(v[q4 * 4 + 1]) * f),
+                           "f"(__uint_as_float(v[q4 * 4 + 2]) * f), "f"(__uint_as_float(v[q4 * 4 + 3]) * f)
+                           : "memory");
+              continue;
+            }
+            float4 o = *ap;
             o.x += __uint_as_float(v[q4 * 4 + 0]) * f;
             o.y += __uint_as_float(v[q4 * 4 + 1]) * f;
             o.z += __uint_as_float(v[q4 * 4 + 2]) * f;
