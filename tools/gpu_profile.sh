@@ -9,9 +9,9 @@ timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_c2_$tag.json
 tail -1 gpurun_out/bench_c2_$tag.json | cut -c1-400
 timeout 900 python bench.py --config C3 --steps 2 --warmup 3 --no-e2e --no-offload > gpurun_out/bench_c3_$tag.json 2> gpurun_out/bench_c3_$tag.err
 tail -1 gpurun_out/bench_c3_$tag.json | cut -c1-300
+fi
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2_$tag.csv \
   python bench.py --steps 1 --warmup 0 --no-e2e --no-offload --no-cpu > /dev/null 2>&1
-fi
 for k in bwd fwd; do
   skip=15; [ $k = bwd ] && skip=0   # chunk 15 = first bwd launch (N-1 .. 0), last fwd launch
   SPPO_TRACE_KIND=$k timeout 900 ncu --set full --clock-control none --import-source on -k regex:${k}_kernel \
