@@ -425,7 +425,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int qpos0 = p.q_start + q0 + g * 64;  // absolute position of this half's column 0
       mbar_wait(&bars.lse_full[s], (m >> 1) & 1);
       mbar_wait(&bars.s_full, m & 1);
+#ifndef SPPO_TRACE_DS
       if (lane == 0 && wq == 0) TR(6 + 4 * g, m);
+#endif
       tc_fence_after();
       // ---- P = exp2(S tau log2e - LSE log2e) for q columns [64g, 64g+64); two 32-column
       //      halves so the second TMEM load overlaps the first half's math
@@ -479,6 +481,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       float2 dp[32];
       tmem_ld32(tPg, *reinterpret_cast<uint32_t(*)[32]>(&dp[0]));
       tmem_wait_ld();
+#ifdef SPPO_TRACE_DS
+      if (lane == 0 && wq == 0 && g == 1) TR(10, m);  // WG1: first dP half in registers
+#endif
       tmem_ld32(tPg + 32, *reinterpret_cast<uint32_t(*)[32]>(&dp[16]));
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -498,13 +503,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           *reinterpret_cast<uint4*>(sDS + sw128(row, ch * 16)) =
               make_uint4(pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
       }
+#ifdef SPPO_TRACE_DS
+      if (lane == 0 && wq == 0 && g == 1) TR(11, m);  // WG1: dS math + stores issued
+#endif
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&bars.delta_empty[s]);  // every thread: its Delta reads are done
       if (!leader) mbar_arrive(&bars.ds_local);  // the peer's own dQ MMA waits on this
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(L_ds_full);
+#ifdef SPPO_TRACE_DS
+      if (lane == 0 && wq == 0 && g == 0) TR(9, m);
+#else
       if (lane == 0 && wq == 0) TR(9 + 2 * g, m);
+#endif
     }
     // ---- epilogue: dK_j, dV_j of this key tile (+= into the fp32 accumulators)
     mbar_wait(&bars.dkdv_done, 0);
