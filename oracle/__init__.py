@@ -44,3 +44,4 @@ from .plan import (  # noqa: F401
     offload_alpha,
     memory_timeline,
 )
+from . import layer  # noqa: F401,E402  (full GPT layer per chunk)

@@ -55,3 +55,48 @@ def ragged_offsets(S: int, N: int, seed: int = 0):
     g = torch.Generator().manual_seed(seed)
     cuts = torch.randperm(S - 1, generator=g)[: N - 1] + 1
     return [0] + sorted(int(c) for c in cuts) + [S]
+
+
+# ---------------------------------------------------------------- full layer
+# Parameter shapes of one GPT layer (hidden H, nn.Linear [out, in] layout); the
+# order matches oracle.layer.PARAM_NAMES.  Recipe:
+# GPT/Megatron initialisation — weights N(0, 0.02), the two projections that
+# feed the residual stream (w_o, w_2) N(0, 0.02/sqrt(2 L)) with L = 32 layers,
+# biases N(0, 0.02), LayerNorm gamma 1 + N(0, 0.1), beta N(0, 0.1); the layer
+# input x and the upstream gradient dz are N(0, 1).  Values are rounded to bf16
+# for bf16 runs.
+LAYER_PARAMS = ("ln1_g", "ln1_b", "w_qkv", "b_qkv", "w_o", "b_o", "ln2_g", "ln2_b", "w_1", "b_1", "w_2", "b_2")
+
+
+def layer_param_shapes(H: int):
+    return {"ln1_g": (H,), "ln1_b": (H,), "w_qkv": (3 * H, H), "b_qkv": (3 * H,), "w_o": (H, H), "b_o": (H,),
+            "ln2_g": (H,), "ln2_b": (H,), "w_1": (4 * H, H), "b_1": (4 * H,), "w_2": (H, 4 * H), "b_2": (H,)}
+
+
+def make_layer_params(H: int, seed: int = 0, dtype=torch.bfloat16, device="cpu", n_layers: int = 32):
+    out = {}
+    g = torch.Generator(device=device)
+    resid_std = 0.02 / (2.0 * n_layers) ** 0.5
+    for n, (name, shape) in enumerate(layer_param_shapes(H).items()):
+        g.manual_seed(int(seed) * 1_000_003 + 7_000_001 + n)
+        x = torch.randn(shape, generator=g, dtype=torch.float32, device=device)
+        if name in ("ln1_g", "ln2_g"):
+            x = 1.0 + 0.1 * x
+        elif name in ("ln1_b", "ln2_b"):
+            x = 0.1 * x
+        elif name in ("w_o", "w_2"):
+            x = resid_std * x
+        else:
+            x = 0.02 * x
+        out[name] = x.to(dtype)
+    return out
+
+
+def make_layer_io(S: int, H: int, seed: int = 0, dtype=torch.bfloat16, device="cpu"):
+    """dict(x, dz) of [S, H] tensors, N(0, 1)."""
+    out = {}
+    for n, name in enumerate(("x", "dz")):
+        g = torch.Generator(device=device)
+        g.manual_seed(int(seed) * 1_000_003 + 9_000_001 + n)
+        out[name] = torch.randn((S, H), generator=g, dtype=torch.float32, device=device).to(dtype)
+    return out
