@@ -107,4 +107,36 @@ cudaError_t launch_bwd_preprocess(const BwdParams& p, bool bf16, cudaStream_t s)
 // dst(dtype) = src(fp32), n elements (n % 4 == 0 fast path).
 cudaError_t launch_cast_f32(const float* src, void* dst, size_t n, bool bf16, cudaStream_t s);
 
+// ---- per-chunk transformer layer (include/sppo_layer.h) ---------------------
+// tcgen05 GEMM: the TMA tensor maps are built on the host (2-D, SWIZZLE_128B):
+// K-major operand [rows][K]: box {64, 128 (A) | BN (B)};  MN-major operand
+// [K][MN]: box {64, 64}.  Epilogue pointers are raw bf16 / fp32.
+struct GemmParams {
+  int32_t M, N, K;
+  int32_t a_mn, b_mn;
+  int32_t a_parts, a_part_w;  // A split along its contiguous dim: width of one part
+  int32_t epi;                // SPPO_EPI_*
+  const void* bias;           // bf16 [N] or null
+  const void* residual;       // bf16 [M][N] or null
+  const void* aux_in;         // bf16 [M][N] (DGELU)
+  void* aux_out;              // bf16 [M][N] (GELU)
+  int32_t c_parts, c_part_w;
+  void* c[3];
+};
+// maps: a[0..a_parts-1], b.  bn = 128 | 256.
+cudaError_t launch_gemm_sm100(const void* tmap_a3, const void* tmap_b, const GemmParams& p, int bn, int num_sms,
+                              cudaStream_t s);
+cudaError_t launch_layernorm_fwd(const void* x, const void* gamma, const void* beta, int64_t rows, int cols,
+                                 float eps, void* y, float* mean, float* rstd, cudaStream_t s);
+cudaError_t launch_layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean,
+                                 const float* rstd, const void* dres, int64_t rows, int cols, void* dx,
+                                 cudaStream_t s);
+cudaError_t launch_col_reduce(int parts, const void* const* dy, const void* x, const float* mean, const float* rstd,
+                              int64_t rows, int cols, float* sum_acc, float* prod_acc, int num_sms,
+                              cudaStream_t s);
+
+// error text for the ABI (thread-local; defined in sppo_api.cu)
+int api_fail(int status, const char* fmt, ...);
+
 }  // namespace sppo
+

@@ -1,0 +1,286 @@
+// Persistent tcgen05 GEMM for the per-chunk transformer layer (
+// include/sppo_layer.h): D[M][N] = sum_k A(m,k) B(k,n), bf16 operands staged by
+// TMA (SWIZZLE_128B) through a kStages-deep shared-memory ring, fp32
+// accumulators in TMEM (two buffers, so the epilogue of tile t overlaps the
+// main loop of tile t+1), fused epilogues (bias, residual add, GELU with the
+// pre-activation saved, GELU backward, fp32 weight-gradient accumulation).
+//
+// CTA = 192 threads, one per SM (grid = min(tiles, #SMs), static round-robin
+// tile schedule, m fastest so concurrently running CTAs share the B tile):
+//   warp 0      TMA producer (one lane)
+//   warp 1      TMEM alloc + MMA issuer (converged warp, one elected lane issues)
+//   warps 2..5  epilogue: warp w reads TMEM lanes 32*(w%4).. (tcgen05.ld 32x32b),
+//               thread = one output row, 32 columns per tcgen05.ld
+// Operand orientation (a_mn / b_mn) selects K-major or MN-major UMMA smem
+// descriptors; the same smem ring serves both (K-major: one box of 64 K x rows;
+// MN-major: boxes of 64 MN x 64 K, 8 KB apart = the descriptor's LBO).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "../../include/sppo_layer.h"
+#include "internal.h"
+#include "sm100_ptx.cuh"
+
+namespace sppo {
+namespace {
+
+using namespace ptx;
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 192;
+constexpr uint32_t kMnBox = 64 * BK * 2;  // 8 KB: one MN-major box (64 MN x 64 K)
+
+template <int BN>
+struct Cfg {
+  static constexpr uint32_t kABytes = BM * BK * 2;
+  static constexpr uint32_t kBBytes = BN * BK * 2;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kSmem = kStages * kStageBytes + 1024;
+  static constexpr uint32_t kTmemCols = 2 * BN;
+};
+
+struct GemmBars {
+  uint64_t full[8], empty[8];
+  uint64_t acc_full[2], acc_empty[2];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ float gelu_f(float u) { return 0.5f * u * (1.f + erff(u * 0.7071067811865476f)); }
+__device__ __forceinline__ float gelu_grad_f(float u) {
+  return 0.5f * (1.f + erff(u * 0.7071067811865476f)) + u * 0.3989422804014327f * __expf(-0.5f * u * u);
+}
+
+__device__ __forceinline__ void load_bf16x32(const void* src, float (&v)[32]) {
+  const uint4* p = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 w = __ldg(p + q);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ws[e]));
+      v[8 * q + 2 * e] = f.x;
+      v[8 * q + 2 * e + 1] = f.y;
+    }
+  }
+}
+
+__device__ __forceinline__ void store_bf16x32(void* dst, const float (&v)[32]) {
+  uint4* p = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    p[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                      pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+}
+
+// Epilogue of 32 consecutive columns [n, n+32) of output row `row`.
+__device__ __forceinline__ void epilogue32(const GemmParams& p, int row, int n, const uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  const int part = n / p.c_part_w;
+  const int col = n - part * p.c_part_w;
+  if (p.epi == SPPO_EPI_ACC_F32) {
+    float4* c = reinterpret_cast<float4*>(static_cast<float*>(p.c[part]) + (size_t)row * p.c_part_w + col);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 t = c[q];
+      t.x += v[4 * q];
+      t.y += v[4 * q + 1];
+      t.z += v[4 * q + 2];
+      t.w += v[4 * q + 3];
+      c[q] = t;
+    }
+    return;
+  }
+  if (p.bias) {
+    float b[32];
+    load_bf16x32(static_cast<const __nv_bfloat16*>(p.bias) + n, b);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] += b[i];
+  }
+  const size_t idx = (size_t)row * p.N + n;
+  if (p.epi == SPPO_EPI_STORE) {
+    if (p.residual) {
+      float x[32];
+      load_bf16x32(static_cast<const __nv_bfloat16*>(p.residual) + idx, x);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += x[i];
+    }
+  } else if (p.epi == SPPO_EPI_GELU) {
+    store_bf16x32(static_cast<__nv_bfloat16*>(p.aux_out) + idx, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
+  } else {  // SPPO_EPI_DGELU
+    float u[32];
+    load_bf16x32(static_cast<const __nv_bfloat16*>(p.aux_in) + idx, u);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(u[i]);
+  }
+  store_bf16x32(static_cast<__nv_bfloat16*>(p.c[part]) + (size_t)row * p.c_part_w + col, v);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
+                const __grid_constant__ CUtensorMap ta2, const __grid_constant__ CUtensorMap tb,
+                const __grid_constant__ GemmParams p) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ GemmBars bars;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = warp_id(), lane = lane_id();
+  const int Mt = (p.M + BM - 1) / BM, Nt = p.N / BN, Kt = (p.K + BK - 1) / BK;
+  const int tiles = Mt * Nt;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&bars.full[s], 1);
+      mbar_init(&bars.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars.acc_full[b], 1);
+      mbar_init(&bars.acc_empty[b], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&ta0);
+    prefetch_tmap(&tb);
+    if (p.a_parts > 1) prefetch_tmap(&ta1);
+    if (p.a_parts > 2) prefetch_tmap(&ta2);
+  }
+  if (warp == 1) tmem_alloc<C::kTmemCols>(&bars.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars.tmem_base;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t % Mt) * BM, n0 = (t / Mt) * BN;
+        for (int kb = 0; kb < Kt; ++kb) {
+          mbar_wait(&bars.empty[stage], phase ^ 1);
+          uint8_t* sA = smem + stage * C::kStageBytes;
+          uint8_t* sB = sA + C::kABytes;
+          mbar_arrive_expect_tx(&bars.full[stage], C::kStageBytes);
+          const int k0 = kb * BK;
+          if (!p.a_mn) {  // A [M][K], split along K
+            const int part = k0 / p.a_part_w;
+            const CUtensorMap* m = part == 0 ? &ta0 : (part == 1 ? &ta1 : &ta2);
+            tma_load_2d(sA, m, &bars.full[stage], k0 - part * p.a_part_w, m0);
+          } else {  // A [K][M], split along M
+            const int part = m0 / p.a_part_w;
+            const CUtensorMap* m = part == 0 ? &ta0 : (part == 1 ? &ta1 : &ta2);
+            const int mc = m0 - part * p.a_part_w;
+#pragma unroll
+            for (int b = 0; b < BM / 64; ++b) tma_load_2d(sA + b * kMnBox, m, &bars.full[stage], mc + 64 * b, k0);
+          }
+          if (!p.b_mn) {
+            tma_load_2d(sB, &tb, &bars.full[stage], k0, n0);
+          } else {
+#pragma unroll
+            for (int b = 0; b < BN / 64; ++b) tma_load_2d(sB + b * kMnBox, &tb, &bars.full[stage], n0 + 64 * b, k0);
+          }
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    const uint32_t idesc = idesc_bf16(BM, BN, p.a_mn, p.b_mn);
+    const uint32_t sbase = smem_u32(smem);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const int buf = it & 1;
+      mbar_wait(&bars.acc_empty[buf], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem + buf * BN;
+      for (int kb = 0; kb < Kt; ++kb) {
+        mbar_wait(&bars.full[stage], phase);
+        tc_fence_after();
+        const uint32_t a_addr = sbase + stage * C::kStageBytes;
+        const uint32_t b_addr = a_addr + C::kABytes;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint64_t ad = p.a_mn ? sdesc_mnmajor(a_addr + k * 2048, kMnBox) : sdesc_kmajor(a_addr + k * 32);
+          const uint64_t bd = p.b_mn ? sdesc_mnmajor(b_addr + k * 2048, kMnBox) : sdesc_kmajor(b_addr + k * 32);
+          mma_ss_w(d, ad, bd, idesc, (kb | k) != 0);
+        }
+        mma_commit_w(&bars.empty[stage]);
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      mma_commit_w(&bars.acc_full[buf]);
+    }
+  } else {
+    // ===================== epilogue =====================
+    const int lane_base = (warp & 3) * 32;
+    int it = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const int buf = it & 1;
+      const int m0 = (t % Mt) * BM, n0 = (t / Mt) * BN;
+      mbar_wait(&bars.acc_full[buf], (it >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + lane_base + lane;
+      const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + buf * BN;
+#pragma unroll 1
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        uint32_t r[32];
+        tmem_ld32(taddr + cc * 32, r);
+        tmem_wait_ld_regs(r);
+        if (cc == BN / 32 - 1) {  // every column of this buffer is in registers: release it
+          tc_fence_before();
+          mbar_arrive(&bars.acc_empty[buf]);
+        }
+        if (row < p.M) epilogue32(p, row, n0 + cc * 32, r);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::kTmemCols>(tmem);
+  }
+}
+
+template <int BN>
+cudaError_t launch_bn(const CUtensorMap* ta, const CUtensorMap* tb, const GemmParams& p, int num_sms,
+                      cudaStream_t s) {
+  using C = Cfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles = ((p.M + BM - 1) / BM) * (p.N / BN);
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  gemm_kernel<BN><<<grid, kThreads, C::kSmem, s>>>(ta[0], ta[1], ta[2], *tb, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_gemm_sm100(const void* tmap_a3, const void* tmap_b, const GemmParams& p, int bn, int num_sms,
+                              cudaStream_t s) {
+  const CUtensorMap* ta = static_cast<const CUtensorMap*>(tmap_a3);
+  const CUtensorMap* tb = static_cast<const CUtensorMap*>(tmap_b);
+  return bn == 256 ? launch_bn<256>(ta, tb, p, num_sms, s) : launch_bn<128>(ta, tb, p, num_sms, s);
+}
+
+}  // namespace sppo

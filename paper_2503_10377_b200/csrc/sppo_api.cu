@@ -264,6 +264,14 @@ void fill_window(const sppo_layout* L, const sppo_kv_set* kv, KvWindow* w) {
 
 }  // namespace
 
+int sppo::api_fail(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return status;
+}
+
 // ================================================================ C ABI
 extern "C" {
 

@@ -29,6 +29,9 @@ EXPORTS = ("sppo_ctx_create", "sppo_ctx_destroy", "sppo_ctx_sync", "sppo_last_er
            "sppo_attn_fwd", "sppo_attn_bwd", "sppo_host_alloc", "sppo_host_free", "sppo_kv_offload",
            "sppo_kv_prefetch", "sppo_partition_equal", "sppo_partition_balanced", "sppo_causal_pairs", "sppo_offload_alpha",
            "sppo_finalize", "sppo_ctx_streams")
+# every symbol include/sppo_layer.h declares (per-chunk transformer layer)
+LAYER_EXPORTS = ("sppo_gemm", "sppo_layernorm_fwd", "sppo_layernorm_bwd", "sppo_col_reduce")
+SPPO_EPI_STORE, SPPO_EPI_GELU, SPPO_EPI_DGELU, SPPO_EPI_ACC_F32 = 0, 1, 2, 3
 
 
 class SppoError(RuntimeError):
@@ -58,6 +61,13 @@ class _BwdArgs(C.Structure):
                 ("dq", C.c_void_p), ("dk", C.c_void_p), ("dv", C.c_void_p)]
 
 
+class _GemmArgs(C.Structure):
+    _fields_ = [("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64), ("a_mn", C.c_int32), ("b_mn", C.c_int32),
+                ("a_parts", C.c_int32), ("a", C.c_void_p * 3), ("b", C.c_void_p), ("epilogue", C.c_int32),
+                ("bias", C.c_void_p), ("residual", C.c_void_p), ("aux_in", C.c_void_p), ("aux_out", C.c_void_p),
+                ("c_parts", C.c_int32), ("c", C.c_void_p * 3)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() (no CPU fallback exists)")
@@ -83,6 +93,10 @@ def _load():
                                 C.POINTER(C.c_double)], i32),
         "sppo_finalize": ([vp, vp, vp, sz, i32, vp], i32),
         "sppo_ctx_streams": ([vp, C.POINTER(vp), C.POINTER(vp)], i32),
+        "sppo_gemm": ([vp, C.POINTER(_GemmArgs), vp], i32),
+        "sppo_layernorm_fwd": ([vp, vp, vp, vp, C.c_int64, i32, C.c_float, vp, vp, vp, vp], i32),
+        "sppo_layernorm_bwd": ([vp, vp, vp, vp, vp, vp, vp, C.c_int64, i32, vp, vp], i32),
+        "sppo_col_reduce": ([vp, i32, C.POINTER(vp), vp, vp, vp, C.c_int64, i32, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -256,3 +270,31 @@ class Context:
 
     def kv_prefetch(self, chunk: int, host: int, dev, nbytes: int, consumer=None, done=None, flags: int = 0):
         _check(_lib.sppo_kv_prefetch(self.h, chunk, host, _ptr(dev), nbytes, _stream(consumer), _event(done), flags))
+
+    # -------------------------------------------------------------- transformer layer (sppo_layer.h)
+    def gemm(self, M: int, N: int, K: int, a, b, c, a_mn: int = 0, b_mn: int = 0, epilogue: int = SPPO_EPI_STORE,
+             bias=None, residual=None, aux_in=None, aux_out=None, stream=None):
+        """sppo_gemm.  ``a`` / ``c``: one tensor or a list of up to 3 (split along the contiguous dim)."""
+        al = list(a) if isinstance(a, (list, tuple)) else [a]
+        cl = list(c) if isinstance(c, (list, tuple)) else [c]
+        g = _GemmArgs(M, N, K, a_mn, b_mn, len(al), (C.c_void_p * 3)(*[_ptr(t) for t in al]), _ptr(b), epilogue,
+                      _ptr(bias), _ptr(residual), _ptr(aux_in), _ptr(aux_out), len(cl),
+                      (C.c_void_p * 3)(*[_ptr(t) for t in cl]))
+        _check(_lib.sppo_gemm(self.h, C.byref(g), _stream(stream)))
+
+    def layernorm_fwd(self, x, gamma, beta, y, mean, rstd, eps: float = 1e-5, stream=None):
+        rows, cols = x.shape
+        _check(_lib.sppo_layernorm_fwd(self.h, _ptr(x), _ptr(gamma), _ptr(beta), rows, cols, eps, _ptr(y),
+                                       _ptr(mean), _ptr(rstd), _stream(stream)))
+
+    def layernorm_bwd(self, dy, x, gamma, mean, rstd, dx, dres=None, stream=None):
+        rows, cols = x.shape
+        _check(_lib.sppo_layernorm_bwd(self.h, _ptr(dy), _ptr(x), _ptr(gamma), _ptr(mean), _ptr(rstd), _ptr(dres),
+                                       rows, cols, _ptr(dx), _stream(stream)))
+
+    def col_reduce(self, dy, rows: int, cols: int, sum_acc, x=None, mean=None, rstd=None, prod_acc=None,
+                   stream=None):
+        dl = list(dy) if isinstance(dy, (list, tuple)) else [dy]
+        arr = (C.c_void_p * len(dl))(*[_ptr(t) for t in dl])
+        _check(_lib.sppo_col_reduce(self.h, len(dl), arr, _ptr(x), _ptr(mean), _ptr(rstd), rows, cols,
+                                    _ptr(sum_acc), _ptr(prod_acc), _stream(stream)))

@@ -14,8 +14,8 @@ from paper_2503_10377_b200 import sppo
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def header_symbols():
-    txt = open(os.path.join(ROOT, "include", "sppo.h")).read()
+def header_symbols(name="sppo.h"):
+    txt = open(os.path.join(ROOT, "include", name)).read()
     return sorted(set(re.findall(r"^\s*(?:sppo_status|const char\*|int32_t)\s+(sppo_\w+)\s*\(", txt, re.M)))
 
 
@@ -27,6 +27,14 @@ def test_library_exports_every_header_symbol():
         assert hasattr(lib, s), s
     assert set(syms) == set(sppo.EXPORTS)
     assert sppo.lib().sppo_version() >= 100
+
+
+def test_library_exports_every_layer_header_symbol():
+    syms = header_symbols("sppo_layer.h")
+    lib = ctypes.CDLL(sppo.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(sppo.LAYER_EXPORTS)
 
 
 def test_partition_and_pairs_match_oracle():
