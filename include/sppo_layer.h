@@ -54,7 +54,8 @@ enum {
  *   [s, 3H] operand); C likewise into c_parts buffers along N (Q|K|V outputs).
  *   Forward y = x W^T: a_mn = 0, b_mn = 0.  Data gradient dx = dy W: a_mn = 0,
  *   b_mn = 1.  Weight gradient dW += dy^T x: a_mn = 1, b_mn = 1, SPPO_EPI_ACC_F32.
- * Shapes: N % 128 == 0, K % 8 == 0, M >= 1 (row tail masked, K tail zero-
+ * Shapes: N % 128 == 0, K % 8 == 0 when K is a contiguous dim (a_mn = 0 or
+ * b_mn = 0), M >= 1 (row tail masked, K tail zero-
  * filled by TMA); a part's width (contiguous elements) % 64 == 0 for a_mn = 0
  * and % 128 == 0 for a_mn = 1; C part width % 128 == 0 (else SPPO_E_SHAPE).
  * bias bf16 [N]; residual, aux_in, aux_out bf16 [M][N] (single buffers).

@@ -65,7 +65,7 @@ sppo_status sppo_gemm(sppo_ctx ctx, const sppo_gemm_args* g, void* stream) {
   if (g->M < 1 || g->N < 1 || g->K < 1) return err(SPPO_E_SHAPE, "gemm: M, N, K must be >= 1");
   if (g->M > INT32_MAX || g->N > INT32_MAX || g->K > INT32_MAX) return err(SPPO_E_SHAPE, "gemm: dims exceed 2^31");
   if (g->N % 128) return err(SPPO_E_SHAPE, "gemm: N = %lld not a multiple of 128", (long long)g->N);
-  if (g->K % 8) return err(SPPO_E_SHAPE, "gemm: K = %lld not a multiple of 8", (long long)g->K);
+  if ((!g->a_mn || !g->b_mn) && g->K % 8) return err(SPPO_E_SHAPE, "gemm: K = %lld not a multiple of 8", (long long)g->K);
   if ((g->a_mn != 0 && g->a_mn != 1) || (g->b_mn != 0 && g->b_mn != 1)) return err(SPPO_E_ARG, "gemm: a_mn/b_mn must be 0|1");
   if (g->a_parts < 1 || g->a_parts > 3 || g->c_parts < 1 || g->c_parts > 3)
     return err(SPPO_E_ARG, "gemm: a_parts / c_parts must be in 1..3");

@@ -1,0 +1,127 @@
+"""GPU parity of the per-chunk GPT layer step (engine_layer.py
+over include/sppo_layer.h + include/sppo.h) against the fp64 oracle
+(oracle/layer.py) on the same bf16 inputs and weights.
+
+Tolerance (reading L17): the GPU path stores every activation in bf16
+(relative rounding 2^-9 = 2.0e-3 per tensor) and chains about ten such
+roundings through the layer forward and twice as many through its backward, so
+the expected relative error per element is a few 1e-3 with tails where
+cancellation makes |ref| small.  The test checks, per tensor,
+  * relative Frobenius error ||gpu - ref|| / ||ref|| <= 1e-2 (forward output z,
+    dx) and <= 2e-2 (parameter gradients: sums over all S tokens), and
+  * elementwise |gpu - ref| <= 5e-2 |ref| + 5e-2 rms(ref).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle.layer as L
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2503_10377_b200 import sppo
+    c = sppo.Context(0)
+    yield c
+    c.close()
+
+
+def _setup(S, H, seed):
+    params = synth.make_layer_params(H, seed)
+    io = synth.make_layer_io(S, H, seed)
+    return params, io
+
+
+def _oracle(params, io, heads):
+    p64 = {k: v.double().numpy() for k, v in params.items()}
+    z, cache = L.layer_fwd(io["x"].double().numpy(), p64, heads)
+    dx, gr = L.layer_bwd(io["dz"].double().numpy(), cache, p64)
+    return z, dx, gr
+
+
+def _check(name, got, ref, frob):
+    got = got.double().cpu().numpy().reshape(ref.shape)
+    rms = np.sqrt(np.mean(ref ** 2))
+    rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
+    err = np.abs(got - ref)
+    bad = err > 5e-2 * np.abs(ref) + 5e-2 * rms
+    assert rel <= frob, f"{name}: relative Frobenius error {rel:.3e} > {frob}"
+    assert not bad.any(), f"{name}: {bad.sum()} elements outside tolerance (max err {err.max():.3e}, rms {rms:.3e})"
+    return rel
+
+
+def _run_and_compare(ctx, S, H, heads, offsets, seed, report=None):
+    from paper_2503_10377_b200 import engine_layer
+    params, io = _setup(S, H, seed)
+    dev = {k: v.cuda() for k, v in params.items()}
+    lay = engine_layer.ChunkedLayer(ctx, H, heads, offsets, dev)
+    out = lay.step(io["x"].cuda(), io["dz"].cuda())
+    torch.cuda.synchronize()
+    z, dx, gr = _oracle(params, io, heads)
+    errs = {"z": _check("z", out["z"], z, 1e-2), "dx": _check("dx", out["dx"], dx, 1e-2)}
+    for k in L.PARAM_NAMES:
+        errs[k] = _check(k, out["grads"][k], gr[k], 2e-2)
+    if report is not None:
+        report.update(errs)
+    return lay, out
+
+
+def test_layer_step_matches_oracle_equal_chunks(ctx):
+    from paper_2503_10377_b200 import sppo
+    errs = {}
+    _run_and_compare(ctx, 1024, 256, 2, sppo.partition_equal(1024, 4), seed=1, report=errs)
+    print("relative Frobenius errors:", {k: f"{v:.2e}" for k, v in errs.items()})
+
+
+def test_layer_step_matches_oracle_ragged_chunks(ctx):
+    _run_and_compare(ctx, 1000, 256, 2, [0, 200, 333, 777, 1000], seed=2)
+
+
+def test_layer_step_wider_hidden(ctx):
+    """H = 512 (4 heads), 3 chunks: every GEMM uses 256-wide N tiles and several K blocks."""
+    _run_and_compare(ctx, 768, 512, 4, [0, 256, 512, 768], seed=3)
+
+
+def test_layer_chunk_count_invariance(ctx):
+    """N = 1 and N = 8 give the same layer (chunking is exact) up to bf16/fp32 rounding."""
+    from paper_2503_10377_b200 import engine_layer, sppo
+    S, H, heads = 1024, 256, 2
+    params, io = _setup(S, H, 4)
+    dev = {k: v.cuda() for k, v in params.items()}
+    outs = []
+    for N in (1, 8):
+        lay = engine_layer.ChunkedLayer(ctx, H, heads, sppo.partition_equal(S, N), dev)
+        o = lay.step(io["x"].cuda(), io["dz"].cuda())
+        outs.append({"z": o["z"].clone(), "dx": o["dx"].clone(), **{k: v.clone() for k, v in o["grads"].items()}})
+    for k in outs[0]:
+        a, b = outs[0][k].double(), outs[1][k].double()
+        rel = (a - b).norm() / b.norm()
+        assert rel < 1e-2, (k, float(rel))
+
+
+def test_layer_type1_offload_poisoned_equals_resident(ctx):
+    """Type-1 activations offloaded with alpha (incl. partial prefixes), device
+    copies poisoned after the D2H: the backward must read the prefetched bytes.
+    Forward outputs are bitwise equal; gradients equal up to fp32 atomics order."""
+    from paper_2503_10377_b200 import engine_layer, sppo
+    S, H, heads = 1024, 256, 2
+    params, io = _setup(S, H, 5)
+    dev = {k: v.cuda() for k, v in params.items()}
+    lay = engine_layer.ChunkedLayer(ctx, H, heads, sppo.partition_equal(S, 4), dev)
+    x, dz = io["x"].cuda(), io["dz"].cuda()
+    ref = lay.step(x, dz)
+    ref = {"z": ref["z"].clone(), "dx": ref["dx"].clone(), **{k: v.clone() for k, v in ref["grads"].items()}}
+    moved = lay.step_offload(x, dz, alpha=[1.0, 0.5, 0.25, 0.0], poison=True)
+    torch.cuda.synchronize()
+    assert moved["d2h"] == moved["h2d"] > 0
+    assert torch.equal(lay.z, ref["z"])
+    assert torch.isfinite(lay.dx.float()).all()
+    for k in ["dx"] + list(L.PARAM_NAMES):
+        got = lay.dx if k == "dx" else lay.grads[k]
+        rel = (got.double() - ref[k].double()).norm() / ref[k].double().norm()
+        assert rel < 1e-5, (k, float(rel))
+    lay.free_host()
