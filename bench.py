@@ -487,6 +487,193 @@ def run_cp(args, cfg, ws, rank, local):
             "note": "kernel roofline / e2e / offload / cpu_baseline: see the default (--parallel heads) line"}
 
 
+# ------------------------------------------------------------------ full layer per chunk
+LAYER_METRIC = "chunked GPT layer fwd+bwd TFLOP/s per B200 (GEMMs + chunked attention), tokens/s"
+
+
+def cpu_oracle_layer_sample(H, heads):
+    """The fp64 layer oracle as it stands on a bounded sample: 512 tokens of the
+    layer (hidden H, `heads` heads) in 2 chunks, forward + reverse-order backward."""
+    import oracle.layer as OL
+    import synth
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([t.get("num_threads", 1) for t in threadpool_info()] or [1])
+    except Exception:
+        cores = os.cpu_count()
+    S_s = 512
+    p = {k: v.double().numpy() for k, v in synth.make_layer_params(H, 0).items()}
+    io = synth.make_layer_io(S_s, H, 0)
+    t0 = time.perf_counter()
+    z, cache = OL.layer_fwd(io["x"].double().numpy(), p, heads, offsets=[0, 256, 512])
+    OL.chunked_layer_bwd(io["dz"].double().numpy(), cache, p)
+    dt = time.perf_counter() - t0
+    f = OL.layer_flops(S_s, H, d=H // heads)
+    fl = sum(f.values())
+    return dict(value=fl / dt / 1e12, cores=int(cores), seconds=dt,
+                sample=f"oracle fp64 layer fwd+bwd, {S_s} tokens (2 chunks), H={H}, {fl:.3e} FLOP in {dt:.1f}s")
+
+
+def run_layer(args, cfg, ws, rank, local):
+    """One step = the GPT layer (hidden = heads*d of the config) forward over the
+    N chunks then backward in reverse (engine_layer.ChunkedLayer).  N > 1 ranks
+    run independent replicas (weak scaling; no collective: the layer has no
+    data-parallel exchange inside the step)."""
+    from paper_2503_10377_b200 import engine_layer, sppo
+    import synth
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    heads, d, S, N = cfg["heads"], cfg["d"], cfg["S"], cfg["N"]
+    H = heads * d
+    ctx = sppo.Context(local)
+    offsets = sppo.partition_balanced(S, N) if args.partition == "balanced" else sppo.partition_equal(S, N)
+    params = synth.make_layer_params(H, 0, device=dev)
+    io = synth.make_layer_io(S, H, 0, device=dev)
+    lay = engine_layer.ChunkedLayer(ctx, H, heads, offsets, params, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        lay.step(io["x"], io["dz"], stream)
+    torch.cuda.synchronize()
+    lay.launches = lay.att.launches = 0
+    barrier(ws)
+    clk = ClockSampler(local)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    phase = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for st in range(args.steps):
+        marks[st].record(stream)
+        lay.step(io["x"], io["dz"], stream, mark=phase[st])
+    marks[args.steps].record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    launches = (lay.launches + lay.att.launches) // args.steps
+    barrier(ws)
+    ms = max_over_ranks(marks[0].elapsed_time(marks[args.steps]) / args.steps, ws)
+    fwd_ms = sum(marks[i].elapsed_time(phase[i]) for i in range(args.steps)) / args.steps
+    bwd_ms = sum(phase[i].elapsed_time(marks[i + 1]) for i in range(args.steps)) / args.steps
+    pairs = sppo.causal_pairs(offsets)
+    f_gemm_fwd, f_attn_fwd = 24 * H * H * S, 4 * d * heads * pairs
+    f_fwd = f_gemm_fwd + f_attn_fwd
+    f_bwd = 2 * f_gemm_fwd + 10 * d * heads * pairs
+    fl = f_fwd + f_bwd
+    peaks = load_peaks()
+    tflops = fl / (ms * 1e-3) / 1e12
+
+    # per-kernel-class device time in one instrumented step (events around each call)
+    lay.timing = True
+    lay.att.timing = True
+    lay.events = {"fwd": [], "bwd": []}
+    lay.att.events = {"fwd": [], "bwd": []}
+    lay.gemm_events = []
+    lay.step(io["x"], io["dz"], stream)
+    torch.cuda.synchronize()
+    gemm_ms = sum(a.elapsed_time(b) for a, b, _ in lay.gemm_events)
+    gemm_fl = sum(f for _, _, f in lay.gemm_events)
+    attn_ms = lay.att.kernel_ms("fwd") + lay.att.kernel_ms("bwd")
+    t_fwd = lay.chunk_ms("fwd")
+    lay.timing = lay.att.timing = False
+    lay.gemm_events = None
+
+    # Type-1 activation offload with sequence-aware alpha vs the paper's fixed full offload
+    offload = None
+    if not args.no_offload:
+        bw = 56.0  # GB/s pinned D2H measured on this pool (profiles/r01/box_probe.json)
+        alpha = lay.alpha_plan(t_fwd, bw)
+
+        def timed(al):
+            res, moved = [], None
+            for rep in range(3):
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                if al is None:
+                    lay.step(io["x"], io["dz"], stream)
+                else:
+                    moved = lay.step_offload(io["x"], io["dz"], al, stream)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                if rep > 0:
+                    res.append(e0.elapsed_time(e1))
+            return statistics.median(res), moved
+
+        res_ms, _ = timed(None)
+        off_ms, moved = timed(alpha)
+        fix_ms, fix_moved = timed([1.0] * (N - 1) + [0.0])
+        A = [lay.type1_bytes(i) for i in range(N)]
+        offload = {"policy": "type1-alpha: a,q,o,y,b,u,g (alpha-prefix) + LSE, LN stats after fwd(i); "
+                             "prefetch depth 2 before bwd(i); K,V resident (Type-0)",
+                   "resident_ms": round(res_ms, 3), "alpha_ms": round(off_ms, 3),
+                   "exposed_pct": round(100 * (off_ms - res_ms) / res_ms, 2),
+                   "d2h_bytes": moved["d2h"], "alpha": [round(a, 3) for a in alpha],
+                   "fixed_alpha1": {"ms": round(fix_ms, 3), "exposed_pct": round(100 * (fix_ms - res_ms) / res_ms, 2),
+                                    "d2h_bytes": fix_moved["d2h"]},
+                   "type1_bytes_per_chunk": A[0], "fwd_ms_per_chunk": [round(t, 3) for t in t_fwd],
+                   "d2h_ms_per_chunk_alpha1": [round(a / bw / 1e6, 3) for a in A], "bw_d2h_gbs_assumed": bw}
+        lay.free_host()
+
+    # e2e: x, dz from pinned host memory in, z, dx back, around one step
+    e2e = None
+    if not args.no_e2e:
+        nb = S * H * 2
+        hin = {t: ctx.host_alloc(nb) for t in ("x", "dz")}
+        hout = {t: ctx.host_alloc(nb) for t in ("z", "dx")}
+        for t in ("x", "dz"):
+            ctx.kv_offload(0, io[t], hin[t], nb, 1.0, producer=stream)
+        ctx.sync()
+        xin = {t: torch.empty_like(io[t]) for t in ("x", "dz")}
+        res = []
+        for rep in range(3):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for t in ("x", "dz"):
+                ctx.kv_prefetch(0, hin[t], xin[t], nb, consumer=stream)
+            out = lay.step(xin["x"], xin["dz"], stream)
+            ev = torch.cuda.Event()
+            ctx.kv_offload(0, out["z"], hout["z"], nb, 1.0, producer=stream)
+            ctx.kv_offload(0, out["dx"], hout["dx"], nb, 1.0, producer=stream, done=ev)
+            stream.wait_event(ev)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if rep > 0:
+                res.append(e0.elapsed_time(e1))
+        e2e_ms = max_over_ranks(statistics.median(res), ws)
+        e2e = {"value": round(fl * ws / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s", "ms_per_step": round(e2e_ms, 3),
+               "h2d_bytes_per_step": 2 * nb * ws, "d2h_bytes_per_step": 2 * nb * ws,
+               "path": "pinned host x, dz -> sppo_kv_prefetch; z, dx -> sppo_kv_offload (not overlapped)"}
+        for ptr in list(hin.values()) + list(hout.values()):
+            ctx.host_free(ptr)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        c = cpu_oracle_layer_sample(H, heads)
+        cpu = {"value": round(c["value"], 6), "unit": "TFLOP/s", "cores": c["cores"], "kind": "oracle",
+               "sample": c["sample"]}
+    gemm_tf = gemm_fl / (gemm_ms * 1e-3) / 1e12
+    line = {"metric": LAYER_METRIC, "value": round(tflops * ws, 2), "unit": "TFLOP/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": cfg["workload"].replace("attention layer", "layer") + " -- full GPT layer "
+                                   f"(hidden {H}, MLP 4x, LayerNorm, GELU) per chunk",
+                       "hidden": H, "heads": heads, "seq_len": S, "chunks": N, "partition": args.partition,
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (activations GBs per step)"},
+            "tokens_per_s": round(S * ws / (ms * 1e-3), 1), "pct_of_bf16_peak": round(100 * tflops / peaks["burst"], 2),
+            "fwd_tflops": round(f_fwd / (fwd_ms * 1e-3) / 1e12, 1), "bwd_tflops": round(f_bwd / (bwd_ms * 1e-3) / 1e12, 1),
+            "breakdown": {"gemm_ms": round(gemm_ms, 3), "gemm_tflops": round(gemm_tf, 1),
+                          "attention_ms": round(attn_ms, 3),
+                          "attention_tflops": round((f_attn_fwd * 3.5) / (attn_ms * 1e-3) / 1e12, 1),
+                          "gemm_flop_share": round(3 * f_gemm_fwd / fl, 3)},
+            "gpu_launches": launches,
+            "roofline": {"bound": "tensor", "kernel": "gemm_kernel (all layer GEMMs, event-timed in one step)",
+                         "achieved": round(gemm_tf, 1), "peak": peaks["burst"], "unit": "TFLOP/s",
+                         "frac": round(gemm_tf / peaks["burst"], 3), "traffic": None,
+                         "peak_source": peaks["source"] + " bf16 burst"},
+            "clocks": clocks, "offload": offload, "e2e": e2e, "cpu_baseline": cpu}
+    ctx.close()
+    return line if rank == 0 else None
+
+
 # ------------------------------------------------------------------ reference arm (the oracle)
 def run_reference(args, cfg, ws, rank):
     if rank != 0:
@@ -526,6 +713,8 @@ def main():
                     help="GB of device memory for the step: picks the KV hot prefix that fits (0: off)")
     ap.add_argument("--partition", default="equal", choices=["equal", "balanced"])
     ap.add_argument("--shard-of", type=int, default=1, help="1 GPU: run rank 0's heads of a G-GPU split")
+    ap.add_argument("--workload", default="attention", choices=["attention", "layer"],
+                    help="attention: the chunked attention hot path (headline); layer: full GPT layer per chunk")
     ap.add_argument("--parallel", default="heads", choices=["heads", "cp"],
                     help="multi-GPU split: heads (no collective in the step) or context-parallel ring")
     args = ap.parse_args()
@@ -535,6 +724,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         line = run_reference(args, cfg, ws, rank)
+    elif args.workload == "layer":
+        line = run_layer(args, cfg, ws, rank, local)
     elif args.parallel == "cp":
         line = run_cp(args, cfg, ws, rank, local)
     else:

@@ -83,6 +83,7 @@ class ChunkedLayer:
         self.grads = {n: torch.zeros(tuple(params[n].shape), **f32) for n in PARAM_NAMES}
         self.launches = 0
         self.events = {"fwd": [], "bwd": []}
+        self.gemm_events = None  # list: (start, end, FLOPs) of every GEMM call (bench instrumentation)
         self._host = {}
 
     # ------------------------------------------------------------------ helpers
@@ -90,8 +91,15 @@ class ChunkedLayer:
         c = self.L.offsets
         return t[c[i]:c[i + 1]]
 
-    def _gemm(self, *args, **kw):
-        self.ctx.gemm(*args, **kw)
+    def _gemm(self, M, N, K, *args, **kw):
+        ev = self.gemm_events
+        if ev is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(kw["stream"])
+        self.ctx.gemm(M, N, K, *args, **kw)
+        if ev is not None:
+            e1.record(kw["stream"])
+            ev.append((e0, e1, 2 * M * N * K))
         self.launches += 1
 
     def _ev(self, kind, stream):
