@@ -126,3 +126,59 @@ def memory_timeline(A, alpha):
         prev = prev + a - shed
         M.append(prev)
     return M
+
+
+# ---------------------------------------------------------------- subsequence pipeline
+def bubble_ratio(p: int, N: int) -> float:
+    """P:282-285 [§3.3 "Inevitable bubble overhead"]: t_b = (p-1) F(N)/N,
+    R_b = (p-1)/N, T = (p-1+N)/N F(N)."""
+    return (p - 1) / N
+
+
+def pipeline_makespan(p: int, N: int, t_fwd: float, t_bwd: float):
+    """Event-driven simulation of the subsequence pipeline: p stages, N chunks;
+    stage s runs fwd(0..N-1) in order, each after stage s-1's fwd of that chunk;
+    then bwd(N-1..0) in order, each after stage s+1's bwd of that chunk (the
+    last stage starts its backward after its own last forward).  Uniform task
+    times.  Returns (makespan, per-stage list of (kind, chunk, start, end))."""
+    fend = [[0.0] * N for _ in range(p)]
+    bend = [[0.0] * N for _ in range(p)]
+    log = [[] for _ in range(p)]
+    for s in range(p):
+        t = 0.0
+        for i in range(N):
+            start = max(t, fend[s - 1][i] if s > 0 else 0.0)
+            t = start + t_fwd
+            fend[s][i] = t
+            log[s].append(("fwd", i, start, t))
+    for s in range(p - 1, -1, -1):
+        t = fend[s][N - 1]
+        for i in range(N - 1, -1, -1):
+            start = max(t, bend[s + 1][i] if s + 1 < p else 0.0)
+            t = start + t_bwd
+            bend[s][i] = t
+            log[s].append(("bwd", i, start, t))
+    return max(bend[s][0] for s in range(p)), log
+
+
+def msp_phases(PP: int, N: int, stage: int):
+    """Multiplexed sequence partitioning (P:420-455 [§6.2]) for pipeline stage
+    `stage`: subsequence ids of the Left-SP, Steady and Right-SP phases and the
+    GPU (stage) ranges that run the two SP phases.
+
+    The Definition's inclusive bounds overlap (Left {0..PP-1-i} and Steady
+    {PP-1-i..N-i} share PP-1-i; Steady reaches N-i, which is Right's first id and
+    equals N for i = 0).  Reading L18: the paper's worked example (Table
+    "multiplexed sequence partitioning for PP=4, N=8", P:386-404) decides:
+        Left = {0 .. PP-2-i},  Steady = {PP-1-i .. N-1-i},  Right = {N-i .. N-1}
+    and the SP ranges follow the Communication-Scope definition
+        Left-SP range = {i .. PP-1}  (empty when Left is empty),
+        Right-SP range = {0 .. i}    (empty when Right is empty)."""
+    if not (1 <= PP and PP <= N and 0 <= stage < PP):
+        raise ValueError("need 1 <= PP <= N and 0 <= stage < PP")
+    left = list(range(0, PP - 1 - stage))
+    steady = list(range(PP - 1 - stage, N - stage))
+    right = list(range(N - stage, N))
+    left_sp = list(range(stage, PP)) if left else []
+    right_sp = list(range(0, stage + 1)) if right else []
+    return dict(left=left, steady=steady, right=right, left_sp=left_sp, right_sp=right_sp)

@@ -31,6 +31,9 @@ EXPORTS = ("sppo_ctx_create", "sppo_ctx_destroy", "sppo_ctx_sync", "sppo_last_er
            "sppo_finalize", "sppo_ctx_streams")
 # every symbol include/sppo_layer.h declares (per-chunk transformer layer)
 LAYER_EXPORTS = ("sppo_gemm", "sppo_layernorm_fwd", "sppo_layernorm_bwd", "sppo_col_reduce")
+# every symbol include/sppo_pipeline.h declares (subsequence pipeline plan)
+PIPELINE_EXPORTS = ("sppo_msp_phases", "sppo_pipeline_bubble")
+SPPO_MSP_LEFT, SPPO_MSP_STEADY, SPPO_MSP_RIGHT = 0, 1, 2
 SPPO_EPI_STORE, SPPO_EPI_GELU, SPPO_EPI_DGELU, SPPO_EPI_ACC_F32 = 0, 1, 2, 3
 
 
@@ -94,6 +97,8 @@ def _load():
         "sppo_finalize": ([vp, vp, vp, sz, i32, vp], i32),
         "sppo_ctx_streams": ([vp, C.POINTER(vp), C.POINTER(vp)], i32),
         "sppo_gemm": ([vp, C.POINTER(_GemmArgs), vp], i32),
+        "sppo_msp_phases": ([i32, i32, i32, C.POINTER(C.c_int8), C.POINTER(i32), C.POINTER(i32)], i32),
+        "sppo_pipeline_bubble": ([i32, i32, C.POINTER(C.c_double)], i32),
         "sppo_layernorm_fwd": ([vp, vp, vp, vp, C.c_int64, i32, C.c_float, vp, vp, vp, vp], i32),
         "sppo_layernorm_bwd": ([vp, vp, vp, vp, vp, vp, vp, C.c_int64, i32, vp, vp], i32),
         "sppo_col_reduce": ([vp, i32, C.POINTER(vp), vp, vp, vp, C.c_int64, i32, vp, vp, vp], i32),
@@ -176,6 +181,23 @@ def offload_alpha(A, m_threshold, last: float = 1.0):
     out = (C.c_double * n)()
     _check(_lib.sppo_offload_alpha(a, m, n, last, out))
     return list(out)
+
+
+def msp_phases(pp: int, n: int, stage: int):
+    """sppo_msp_phases -> dict(left, steady, right ids; left_sp, right_sp stage lists)."""
+    ph = (C.c_int8 * n)()
+    ls, rs = (C.c_int32 * 2)(), (C.c_int32 * 2)()
+    _check(_lib.sppo_msp_phases(pp, n, stage, ph, ls, rs))
+    ids = {k: [x for x in range(n) if ph[x] == c] for k, c in (("left", 0), ("steady", 1), ("right", 2))}
+    ids["left_sp"] = list(range(ls[0], ls[1] + 1))
+    ids["right_sp"] = list(range(rs[0], rs[1] + 1))
+    return ids
+
+
+def pipeline_bubble(pp: int, n: int) -> float:
+    out = C.c_double()
+    _check(_lib.sppo_pipeline_bubble(pp, n, C.byref(out)))
+    return out.value
 
 
 class Layout:

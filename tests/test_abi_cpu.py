@@ -37,6 +37,14 @@ def test_library_exports_every_layer_header_symbol():
     assert set(syms) == set(sppo.LAYER_EXPORTS)
 
 
+def test_library_exports_every_pipeline_header_symbol():
+    syms = header_symbols("sppo_pipeline.h")
+    lib = ctypes.CDLL(sppo.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(sppo.PIPELINE_EXPORTS)
+
+
 def test_partition_and_pairs_match_oracle():
     for S, N in [(1024, 4), (131072, 16), (10, 3), (5, 5), (1048576, 64), (7, 1)]:
         off = sppo.partition_equal(S, N)
