@@ -571,7 +571,18 @@ def run_layer(args, cfg, ws, rank, local):
     gemm_fl = sum(f for _, _, f in lay.gemm_events)
     attn_ms = lay.att.kernel_ms("fwd") + lay.att.kernel_ms("bwd")
     t_fwd = lay.chunk_ms("fwd")
+    t_bwd = list(reversed(lay.chunk_ms("bwd")))  # recorded N-1..0 -> index by chunk
     lay.timing = lay.att.timing = False
+    # subsequence pipeline model: PP stages of one such layer each, the
+    # measured per-chunk times on every stage; makespan from sppo_pipeline_makespan
+    F = sum(t_fwd) + sum(t_bwd)
+    pipe = {"note": "MODEL from this run's measured per-chunk layer fwd/bwd times (1 layer per stage); "
+                    "multi-GPU execution not measured (one GPU in this environment)",
+            "F_ms": round(F, 3)}
+    for pp in (2, 4, 8):
+        T = sppo.pipeline_makespan(pp, t_fwd, t_bwd)
+        pipe[f"pp{pp}"] = {"makespan_ms": round(T, 3), "bubble_ratio": round((T - F) / F, 4),
+                           "uniform_formula": round(sppo.pipeline_bubble(pp, N), 4)}
     lay.gemm_events = None
 
     # Type-1 activation offload with sequence-aware alpha vs the paper's fixed full offload
@@ -669,7 +680,7 @@ def run_layer(args, cfg, ws, rank, local):
                          "achieved": round(gemm_tf, 1), "peak": peaks["burst"], "unit": "TFLOP/s",
                          "frac": round(gemm_tf / peaks["burst"], 3), "traffic": None,
                          "peak_source": peaks["source"] + " bf16 burst"},
-            "clocks": clocks, "offload": offload, "e2e": e2e, "cpu_baseline": cpu}
+            "clocks": clocks, "offload": offload, "pipeline_model": pipe, "e2e": e2e, "cpu_baseline": cpu}
     ctx.close()
     return line if rank == 0 else None
 

@@ -34,6 +34,15 @@ enum { SPPO_MSP_LEFT = 0, SPPO_MSP_STEADY = 1, SPPO_MSP_RIGHT = 2 };
 sppo_status sppo_msp_phases(int32_t pp, int32_t n, int32_t stage, int8_t* phase_out, int32_t* left_sp,
                             int32_t* right_sp);
 
+/* Makespan of one step of the subsequence pipeline: pp stages
+ * with identical per-chunk times t_fwd[i], t_bwd[i] (host arrays, n entries);
+ * stage s runs fwd(i) for i = 0..n-1, each after stage s-1's fwd(i), then
+ * bwd(i) for i = n-1..0, each after stage s+1's bwd(i) (the last stage starts
+ * its backward after its last forward).  With uniform times this is
+ * (pp-1+n)/n * F(n).  Writes the makespan (same unit as the inputs). */
+sppo_status sppo_pipeline_makespan(int32_t pp, int32_t n, const double* t_fwd, const double* t_bwd,
+                                   double* makespan_out);
+
 /* R_b = (pp - 1) / n. */
 sppo_status sppo_pipeline_bubble(int32_t pp, int32_t n, double* ratio_out);
 

@@ -135,12 +135,15 @@ def bubble_ratio(p: int, N: int) -> float:
     return (p - 1) / N
 
 
-def pipeline_makespan(p: int, N: int, t_fwd: float, t_bwd: float):
+def pipeline_makespan(p: int, N: int, t_fwd, t_bwd):
     """Event-driven simulation of the subsequence pipeline: p stages, N chunks;
     stage s runs fwd(0..N-1) in order, each after stage s-1's fwd of that chunk;
     then bwd(N-1..0) in order, each after stage s+1's bwd of that chunk (the
-    last stage starts its backward after its own last forward).  Uniform task
-    times.  Returns (makespan, per-stage list of (kind, chunk, start, end))."""
+    last stage starts its backward after its own last forward).  Task times are
+    scalars (uniform) or per-chunk lists.  Returns (makespan, per-stage list of
+    (kind, chunk, start, end))."""
+    tf = list(t_fwd) if hasattr(t_fwd, "__len__") else [t_fwd] * N
+    tb = list(t_bwd) if hasattr(t_bwd, "__len__") else [t_bwd] * N
     fend = [[0.0] * N for _ in range(p)]
     bend = [[0.0] * N for _ in range(p)]
     log = [[] for _ in range(p)]
@@ -148,14 +151,14 @@ def pipeline_makespan(p: int, N: int, t_fwd: float, t_bwd: float):
         t = 0.0
         for i in range(N):
             start = max(t, fend[s - 1][i] if s > 0 else 0.0)
-            t = start + t_fwd
+            t = start + tf[i]
             fend[s][i] = t
             log[s].append(("fwd", i, start, t))
     for s in range(p - 1, -1, -1):
         t = fend[s][N - 1]
         for i in range(N - 1, -1, -1):
             start = max(t, bend[s + 1][i] if s + 1 < p else 0.0)
-            t = start + t_bwd
+            t = start + tb[i]
             bend[s][i] = t
             log[s].append(("bwd", i, start, t))
     return max(bend[s][0] for s in range(p)), log

@@ -32,7 +32,7 @@ EXPORTS = ("sppo_ctx_create", "sppo_ctx_destroy", "sppo_ctx_sync", "sppo_last_er
 # every symbol include/sppo_layer.h declares (per-chunk transformer layer)
 LAYER_EXPORTS = ("sppo_gemm", "sppo_layernorm_fwd", "sppo_layernorm_bwd", "sppo_col_reduce")
 # every symbol include/sppo_pipeline.h declares (subsequence pipeline plan)
-PIPELINE_EXPORTS = ("sppo_msp_phases", "sppo_pipeline_bubble")
+PIPELINE_EXPORTS = ("sppo_msp_phases", "sppo_pipeline_bubble", "sppo_pipeline_makespan")
 SPPO_MSP_LEFT, SPPO_MSP_STEADY, SPPO_MSP_RIGHT = 0, 1, 2
 SPPO_EPI_STORE, SPPO_EPI_GELU, SPPO_EPI_DGELU, SPPO_EPI_ACC_F32 = 0, 1, 2, 3
 
@@ -99,6 +99,8 @@ def _load():
         "sppo_gemm": ([vp, C.POINTER(_GemmArgs), vp], i32),
         "sppo_msp_phases": ([i32, i32, i32, C.POINTER(C.c_int8), C.POINTER(i32), C.POINTER(i32)], i32),
         "sppo_pipeline_bubble": ([i32, i32, C.POINTER(C.c_double)], i32),
+        "sppo_pipeline_makespan": ([i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double)], i32),
         "sppo_layernorm_fwd": ([vp, vp, vp, vp, C.c_int64, i32, C.c_float, vp, vp, vp, vp], i32),
         "sppo_layernorm_bwd": ([vp, vp, vp, vp, vp, vp, vp, C.c_int64, i32, vp, vp], i32),
         "sppo_col_reduce": ([vp, i32, C.POINTER(vp), vp, vp, vp, C.c_int64, i32, vp, vp, vp], i32),
@@ -197,6 +199,13 @@ def msp_phases(pp: int, n: int, stage: int):
 def pipeline_bubble(pp: int, n: int) -> float:
     out = C.c_double()
     _check(_lib.sppo_pipeline_bubble(pp, n, C.byref(out)))
+    return out.value
+
+
+def pipeline_makespan(pp: int, t_fwd, t_bwd) -> float:
+    n = len(t_fwd)
+    out = C.c_double()
+    _check(_lib.sppo_pipeline_makespan(pp, n, (C.c_double * n)(*t_fwd), (C.c_double * n)(*t_bwd), C.byref(out)))
     return out.value
 
 

@@ -36,6 +36,18 @@ def test_bubble_ratio_paper_example_and_simulation():
                    [("bwd", i) for i in range(N - 1, -1, -1)]
 
 
+def test_makespan_helper_matches_simulation_nonuniform():
+    import random
+    rnd = random.Random(3)
+    for p, N in [(1, 1), (2, 8), (4, 16), (8, 5)]:
+        tf = [rnd.uniform(0.5, 3.0) for _ in range(N)]
+        tb = [2.5 * t for t in tf]
+        T, _ = plan.pipeline_makespan(p, N, tf, tb)
+        assert abs(sppo.pipeline_makespan(p, tf, tb) - T) < 1e-9 * T
+    # uniform: (p-1+N)/N F(N)
+    assert abs(sppo.pipeline_makespan(4, [1.0] * 16, [2.0] * 16) - 19 * 3.0) < 1e-12
+
+
 def test_msp_phases_match_paper_table():
     g = GOLD["msp_table_pp4_n8"]
     for s, row in enumerate(g["stages"]):
