@@ -6,7 +6,7 @@
 // pre-activation saved, GELU backward, fp32 weight-gradient accumulation).
 //
 // CTA = 192 threads, one per SM (grid = min(tiles, #SMs), static round-robin
-// tile schedule, m fastest so concurrently running CTAs share the B tile):
+// tile schedule in grouped raster order, tile_coords()):
 //   warp 0      TMA producer (one lane)
 //   warp 1      TMEM alloc + MMA issuer (converged warp, one elected lane issues)
 //   warps 2..5  epilogue: warp w reads TMEM lanes 32*(w%4).. (tcgen05.ld 32x32b),
@@ -46,6 +46,19 @@ struct GemmBars {
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
 };
+
+// Tile t -> (m block, n block), grouped raster: kGroupM consecutive m blocks sweep
+// the n blocks together, so the CTAs running at one time share a few A row panels
+// and B column panels (L2 reuse) instead of all of A.
+constexpr int kGroupM = 8;
+__device__ __forceinline__ void tile_coords(int t, int Mt, int Nt, int& mb, int& nb) {
+  const int per_group = kGroupM * Nt;
+  const int g = t / per_group, r = t - g * per_group;
+  const int m_first = g * kGroupM;
+  const int gm = min(Mt - m_first, kGroupM);
+  mb = m_first + r % gm;
+  nb = r / gm;
+}
 
 __device__ __forceinline__ float gelu_f(float u) { return 0.5f * u * (1.f + erff(u * 0.7071067811865476f)); }
 __device__ __forceinline__ float gelu_grad_f(float u) {
@@ -164,7 +177,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int m0 = (t % Mt) * BM, n0 = (t / Mt) * BN;
+        int mb, nb;
+        tile_coords(t, Mt, Nt, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
         for (int kb = 0; kb < Kt; ++kb) {
           mbar_wait(&bars.empty[stage], phase ^ 1);
           uint8_t* sA = smem + stage * C::kStageBytes;
@@ -232,7 +247,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const int buf = it & 1;
-      const int m0 = (t % Mt) * BM, n0 = (t / Mt) * BN;
+      int mb, nb;
+      tile_coords(t, Mt, Nt, mb, nb);
+      const int m0 = mb * BM, n0 = nb * BN;
       mbar_wait(&bars.acc_full[buf], (it >> 1) & 1);
       tc_fence_after();
       const int row = m0 + lane_base + lane;
@@ -258,6 +275,176 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- CTA-pair variant
+// Cluster of 2 CTAs shares one 256 x 256 tile: tcgen05.mma.cta_group::2 M=256
+// N=256 issued by the leader; CTA r holds A rows [128r, 128r+128) and B columns
+// [128r, 128r+128) of the tile in its own smem (half of B per SM: 32 KB of
+// operands per 64-deep K block instead of 48 KB), its TMEM receives its 128 D
+// rows x 256 columns.  Both CTAs' TMA loads complete on the leader's full
+// barrier; MMA commits multicast to both CTAs; both CTAs' epilogue threads
+// release an accumulator buffer on the leader's acc_empty barrier.
+constexpr int kPairStages = 6;
+constexpr uint32_t kPairA = 128 * BK * 2, kPairB = 128 * BK * 2, kPairStage = kPairA + kPairB;
+constexpr int kPairSmem = kPairStages * kPairStage + 1024;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
+                 const __grid_constant__ CUtensorMap ta2, const __grid_constant__ CUtensorMap tb,
+                 const __grid_constant__ GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ GemmBars bars;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int Mt = (p.M + 255) / 256, Nt = p.N / 256, Kt = (p.K + BK - 1) / BK;
+  const int tiles = Mt * Nt;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPairStages; ++s) {
+      mbar_init(&bars.full[s], 1);
+      mbar_init(&bars.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars.acc_full[b], 1);
+      mbar_init(&bars.acc_empty[b], 256);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&ta0);
+    prefetch_tmap(&tb);
+    if (p.a_parts > 1) prefetch_tmap(&ta1);
+    if (p.a_parts > 2) prefetch_tmap(&ta2);
+  }
+  if (warp == 1) tmem_alloc_pair<512>(&bars.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = bars.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < tiles; t += ncl) {
+        int mb, nb;
+        tile_coords(t, Mt, Nt, mb, nb);
+        const int m0 = mb * 256 + 128 * (int)rank, n0 = nb * 256 + 128 * (int)rank;
+        for (int kb = 0; kb < Kt; ++kb) {
+          mbar_wait(&bars.empty[stage], phase ^ 1);
+          uint8_t* sA = smem + stage * kPairStage;
+          uint8_t* sB = sA + kPairA;
+          if (leader) mbar_arrive_expect_tx(&bars.full[stage], 2 * kPairStage);
+          const uint32_t Lf = mapa(smem_u32(&bars.full[stage]), 0);
+          const int k0 = kb * BK;
+          if (!p.a_mn) {
+            const int part = k0 / p.a_part_w;
+            const CUtensorMap* m = part == 0 ? &ta0 : (part == 1 ? &ta1 : &ta2);
+            tma_load_2d_pair(sA, m, Lf, k0 - part * p.a_part_w, m0);
+          } else {
+            const int part = m0 / p.a_part_w;
+            const CUtensorMap* m = part == 0 ? &ta0 : (part == 1 ? &ta1 : &ta2);
+            const int mc = m0 - part * p.a_part_w;
+            tma_load_2d_pair(sA, m, Lf, mc, k0);
+            tma_load_2d_pair(sA + kMnBox, m, Lf, mc + 64, k0);
+          }
+          if (!p.b_mn) {
+            tma_load_2d_pair(sB, &tb, Lf, k0, n0);
+          } else {
+            tma_load_2d_pair(sB, &tb, Lf, n0, k0);
+            tma_load_2d_pair(sB + kMnBox, &tb, Lf, n0 + 64, k0);
+          }
+          if (++stage == kPairStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      const uint32_t idesc = idesc_bf16(256, 256, p.a_mn, p.b_mn);
+      const uint32_t sbase = smem_u32(smem);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cid; t < tiles; t += ncl, ++it) {
+        const int buf = it & 1;
+        mbar_wait(&bars.acc_empty[buf], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + buf * 256;
+        for (int kb = 0; kb < Kt; ++kb) {
+          mbar_wait(&bars.full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = sbase + stage * kPairStage;
+          const uint32_t b_addr = a_addr + kPairA;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = p.a_mn ? sdesc_mnmajor(a_addr + k * 2048, kMnBox) : sdesc_kmajor(a_addr + k * 32);
+            const uint64_t bd = p.b_mn ? sdesc_mnmajor(b_addr + k * 2048, kMnBox) : sdesc_kmajor(b_addr + k * 32);
+            mma2_ss_w(d, ad, bd, idesc, (kb | k) != 0);
+          }
+          mma2_commit_w(&bars.empty[stage]);
+          if (++stage == kPairStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma2_commit_w(&bars.acc_full[buf]);
+      }
+    }
+  } else {
+    const int lane_base = (warp & 3) * 32;
+    int it = 0;
+    for (int t = cid; t < tiles; t += ncl, ++it) {
+      const int buf = it & 1;
+      int mb, nb;
+      tile_coords(t, Mt, Nt, mb, nb);
+      const int m0 = mb * 256 + 128 * (int)rank, n0 = nb * 256;
+      mbar_wait(&bars.acc_full[buf], (it >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + lane_base + lane;
+      const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + buf * 256;
+      const uint32_t Le = mapa(smem_u32(&bars.acc_empty[buf]), 0);
+#pragma unroll 1
+      for (int cc = 0; cc < 8; ++cc) {
+        uint32_t r[32];
+        tmem_ld32(taddr + cc * 32, r);
+        tmem_wait_ld_regs(r);
+        if (cc == 7) {
+          tc_fence_before();
+          mbar_arrive_cluster(Le);
+        }
+        if (row < p.M) epilogue32(p, row, n0 + cc * 32, r);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem);
+  }
+}
+
+cudaError_t launch_pair(const CUtensorMap* ta, const CUtensorMap* tb, const GemmParams& p, int num_sms,
+                        cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles = ((p.M + 255) / 256) * (p.N / 256);
+  const int clusters = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  gemm2_kernel<<<2 * clusters, kThreads, kPairSmem, s>>>(ta[0], ta[1], ta[2], *tb, p);
+  return cudaGetLastError();
+}
+
 template <int BN>
 cudaError_t launch_bn(const CUtensorMap* ta, const CUtensorMap* tb, const GemmParams& p, int num_sms,
                       cudaStream_t s) {
@@ -280,6 +467,7 @@ cudaError_t launch_gemm_sm100(const void* tmap_a3, const void* tmap_b, const Gem
                               cudaStream_t s) {
   const CUtensorMap* ta = static_cast<const CUtensorMap*>(tmap_a3);
   const CUtensorMap* tb = static_cast<const CUtensorMap*>(tmap_b);
+  if (bn == 2256) return launch_pair(ta, tb, p, num_sms, s);
   return bn == 256 ? launch_bn<256>(ta, tb, p, num_sms, s) : launch_bn<128>(ta, tb, p, num_sms, s);
 }
 

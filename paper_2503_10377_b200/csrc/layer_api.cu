@@ -3,6 +3,7 @@
 // the kernel by value as __grid_constant__ parameters), dispatch.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -96,7 +97,17 @@ sppo_status sppo_gemm(sppo_ctx ctx, const sppo_gemm_args* g, void* stream) {
     if (q && !al16(q)) return err(SPPO_E_ALIGN, "gemm: epilogue operand not 16-byte aligned");
 
   const int64_t cpw = g->N / g->c_parts;
-  const int bn = (cpw % 256 == 0) ? 256 : 128;
+  int bn = (cpw % 256 == 0) ? 256 : 128;
+  // CTA pair (cluster of 2, 256 x 256 tiles) when N tiles are 256 wide, M spans
+  // more than one 128-row tile and both operands are K-major (measured at the
+  // GPT-7B chunk shapes, tools/gemm_bench.py: pair 1395-1403 vs single 1307-1314
+  // TF/s for x W^T; with an MN-major operand the pair was slower, 1063-1152 vs
+  // 1190-1318).  SPPO_GEMM_PAIR=0 / 2 forces the single-CTA / pair kernel.
+  static const int pair_env = [] {
+    const char* e = getenv("SPPO_GEMM_PAIR");
+    return e ? atoi(e) : 1;
+  }();
+  const bool pair = bn == 256 && g->M > 128 && (pair_env == 2 || (pair_env == 1 && !g->a_mn && !g->b_mn));
   CUtensorMap ta[3], tb;
   memset(ta, 0, sizeof ta);
   for (int i = 0; i < g->a_parts; ++i) {
@@ -105,7 +116,7 @@ sppo_status sppo_gemm(sppo_ctx ctx, const sppo_gemm_args* g, void* stream) {
   }
   for (int i = g->a_parts; i < 3; ++i) ta[i] = ta[0];
   {
-    sppo_status s = g->b_mn ? encode2d(&tb, g->b, g->K, g->N, 64) : encode2d(&tb, g->b, g->N, g->K, bn);
+    sppo_status s = g->b_mn ? encode2d(&tb, g->b, g->K, g->N, 64) : encode2d(&tb, g->b, g->N, g->K, pair ? 128 : bn);
     if (s != SPPO_OK) return s;
   }
   GemmParams p{};
@@ -124,7 +135,7 @@ sppo_status sppo_gemm(sppo_ctx ctx, const sppo_gemm_args* g, void* stream) {
   p.c_parts = g->c_parts;
   p.c_part_w = (int32_t)cpw;
   for (int i = 0; i < 3; ++i) p.c[i] = i < g->c_parts ? g->c[i] : g->c[0];
-  cudaError_t e = launch_gemm_sm100(ta, &tb, p, bn, sm_count(), (cudaStream_t)stream);
+  cudaError_t e = launch_gemm_sm100(ta, &tb, p, pair ? 2256 : bn, sm_count(), (cudaStream_t)stream);
   if (e != cudaSuccess) return err(SPPO_E_CUDA, "gemm launch: %s", cudaGetErrorString(e));
   return SPPO_OK;
 }

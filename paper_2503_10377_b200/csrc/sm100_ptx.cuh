@@ -380,6 +380,15 @@ __device__ __forceinline__ void tma_load_3d_pair(void* dst, const void* tmap, ui
       "l"(tmap), "r"(bar_c), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// 2-D TMA tile load into this CTA's smem, completion counted on the mbarrier at
+// shared::cluster address `bar_c` (the pair leader's).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, uint32_t bar_c, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(bar_c), "r"(c0), "r"(c1)
+      : "memory");
+}
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem) {  // one warp in each CTA of the pair
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
