@@ -535,7 +535,7 @@ def run_layer(args, cfg, ws, rank, local):
     for _ in range(args.warmup):
         lay.step(io["x"], io["dz"], stream)
     torch.cuda.synchronize()
-    lay.launches = lay.att.launches = 0
+    lay.launches = 0
     barrier(ws)
     clk = ClockSampler(local)
     marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
@@ -546,7 +546,7 @@ def run_layer(args, cfg, ws, rank, local):
     marks[args.steps].record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
-    launches = (lay.launches + lay.att.launches) // args.steps
+    launches = lay.launches // args.steps
     barrier(ws)
     ms = max_over_ranks(marks[0].elapsed_time(marks[args.steps]) / args.steps, ws)
     fwd_ms = sum(marks[i].elapsed_time(phase[i]) for i in range(args.steps)) / args.steps
@@ -561,18 +561,17 @@ def run_layer(args, cfg, ws, rank, local):
 
     # per-kernel-class device time in one instrumented step (events around each call)
     lay.timing = True
-    lay.att.timing = True
     lay.events = {"fwd": [], "bwd": []}
-    lay.att.events = {"fwd": [], "bwd": []}
-    lay.gemm_events = []
+    lay.gemm_events, lay.attn_events = [], []
     lay.step(io["x"], io["dz"], stream)
     torch.cuda.synchronize()
     gemm_ms = sum(a.elapsed_time(b) for a, b, _ in lay.gemm_events)
     gemm_fl = sum(f for _, _, f in lay.gemm_events)
-    attn_ms = lay.att.kernel_ms("fwd") + lay.att.kernel_ms("bwd")
+    attn_ms = sum(a.elapsed_time(b) for a, b in lay.attn_events)
     t_fwd = lay.chunk_ms("fwd")
     t_bwd = list(reversed(lay.chunk_ms("bwd")))  # recorded N-1..0 -> index by chunk
-    lay.timing = lay.att.timing = False
+    lay.timing = False
+    lay.attn_events = None
     # subsequence pipeline model: PP stages of one such layer each, the
     # measured per-chunk times on every stage; makespan from sppo_pipeline_makespan
     F = sum(t_fwd) + sum(t_bwd)

@@ -6,7 +6,7 @@ i = N-1..0 (reading L11).  Per chunk i (token rows [c_i, c_{i+1}))
 
   forward   a = LN1(x)                       sppo_layernorm_fwd
             [q k v] = a W_qkv^T + b_qkv      sppo_gemm (C split into Q | K | V)
-            o = attention(q; K, V of 0..i)   sppo_attn_fwd  (ChunkedAttention)
+            o = attention(q; K, V of 0..i)   sppo_attn_fwd
             y = x + o W_o^T + b_o            sppo_gemm (bias + residual epilogue)
             b = LN2(y)                       sppo_layernorm_fwd
             g = GELU(u), u = b W_1^T + b_1   sppo_gemm (GELU epilogue, u saved)
@@ -21,13 +21,22 @@ i = N-1..0 (reading L11).  Per chunk i (token rows [c_i, c_{i+1}))
             dx = dy + LN1_bwd(da)
 
 Two-level activation management (P:356 [§5.1]): K_i, V_i stay on the GPU
-(Type-0); the Type-1 tensors of chunk i — a, q, o, y, b, u, g (13 h bf16 per
-token) plus LSE and the LayerNorm statistics — leave after fwd(i) as the
-alpha_i-prefix of each token-major buffer on the ctx D2H stream (overlapping
-fwd(i+1)) and come back on the H2D stream before bwd(i), at most
-``depth`` chunks ahead.  alpha_i = min(1, BW_D2H * T_fwd(i+1) / A_i),
-alpha_{N-1} = 0 (reading L9).  This module allocates buffers and
-sequences ABI calls; every arithmetic step runs in libsppo's kernels.
+(Type-0, whole-sequence buffers); the Type-1 tensors of chunk i — a, q, o, y, b,
+u, g (13 h bf16 per token) plus LSE and the LayerNorm statistics — live in a
+per-chunk set.  Under step_offload they leave after fwd(i) as the
+alpha_i-prefix of each tensor on the ctx D2H stream (overlapping fwd(i+1),
+P:369) and come back on the H2D stream before bwd(i), at most ``depth`` chunks
+ahead (P:356); alpha_i = min(1, BW_D2H * T_fwd(i+1) / A_i), alpha_{N-1} = 0
+(reading L9).
+
+Memory (``pool``): False = one whole-sequence buffer per Type-1 tensor (chunk
+sets are row views; offload then only measures overlap).  True = chunk sets are
+separate allocations: once the D2H of chunk i's prefix has completed, the
+device copy is released (the suffix, 1 - alpha_i, is kept as a compact copy),
+and the backward re-allocates the set, prefetches the prefix and restores the
+suffix — so device memory holds K/V, the resident suffixes and a few in-flight
+sets instead of every chunk's activations.  Buffers are torch allocations; every
+arithmetic step runs in libsppo's kernels.
 """
 
 from __future__ import annotations
@@ -35,61 +44,82 @@ from __future__ import annotations
 import torch
 
 from . import sppo
-from .engine import ChunkedAttention
 
 PARAM_NAMES = ("ln1_g", "ln1_b", "w_qkv", "b_qkv", "w_o", "b_o", "ln2_g", "ln2_b", "w_1", "b_1", "w_2", "b_2")
 TYPE1 = ("a", "q", "o", "y", "b", "u", "g")  # token-major bf16 activations offloaded with alpha
-STATS = ("mu1", "rstd1", "mu2", "rstd2")     # fp32 [S] per-token LayerNorm statistics (offloaded whole)
+STATS = ("lse", "mu1", "rstd1", "mu2", "rstd2")  # fp32 statistics, offloaded whole
 LN_EPS = 1e-5
 
 
 class ChunkedLayer:
     def __init__(self, ctx: sppo.Context, hidden: int, heads: int, offsets, params: dict, device="cuda",
-                 timing: bool = False):
+                 timing: bool = False, pool: bool = False):
         self.ctx = ctx
         self.H, self.heads = hidden, heads
         self.d = hidden // heads
         self.L = sppo.Layout(heads, self.d, offsets, dtype=sppo.SPPO_BF16)
         self.N = self.L.num_chunks
+        if self.N > 256:
+            raise ValueError("ChunkedLayer issues one attention window per chunk: N <= 256")
         self.S = S = self.L.offsets[-1]
         self.device = torch.device(device)
         self.p = params
         self.timing = timing
+        self.pool = pool
         H = hidden
         bf = dict(dtype=torch.bfloat16, device=self.device)
         f32 = dict(dtype=torch.float32, device=self.device)
-        self.att = ChunkedAttention(ctx, self.L, device=device, fwd_streams=1)
-        # saved activations (whole sequence, token-major; chunk i = rows [c_i, c_{i+1}))
-        self.a = torch.empty((S, H), **bf)
-        self.q = torch.empty((S, H), **bf)
+        # Type-0 (resident) and outputs: whole sequence, token-major
         self.k = torch.empty((S, H), **bf)
         self.v = torch.empty((S, H), **bf)
-        self.o = self.att.o.view(S, H)
-        self.y = torch.empty((S, H), **bf)
-        self.b = torch.empty((S, H), **bf)
-        self.u = torch.empty((S, 4 * H), **bf)
-        self.g = torch.empty((S, 4 * H), **bf)
         self.z = torch.empty((S, H), **bf)
-        for n in STATS:
-            setattr(self, n, torch.empty((S,), **f32))
-        # backward: outputs and per-chunk scratch (longest chunk)
-        smax = max(self.L.chunk_len(i) for i in range(self.N))
         self.dx = torch.empty((S, H), **bf)
-        self.d_o = torch.empty((S, H), **bf)
+        self.dk_acc = torch.empty((S, H), **f32)
+        self.dv_acc = torch.empty((S, H), **f32)
+        # per-chunk backward scratch (longest chunk)
+        smax = max(self.L.chunk_len(i) for i in range(self.N))
         self.du = torch.empty((smax, 4 * H), **bf)
-        self.dbn = torch.empty((smax, H), **bf)
-        self.dy = torch.empty((smax, H), **bf)
-        self.da = torch.empty((smax, H), **bf)
+        for n in ("dbn", "dy", "da", "d_o", "dq", "dkc", "dvc"):
+            setattr(self, n, torch.empty((smax, H), **bf))
+        self.dq_acc = torch.empty((smax, H), **f32)
+        self.delta = torch.empty((smax * heads,), **f32)
+        # Type-1: whole-sequence buffers (resident) or per-chunk allocations (pool)
+        self._full = None
+        if not pool:
+            self._full = {n: torch.empty((S, 4 * H if n in ("u", "g") else H), **bf) for n in TYPE1}
+            self._full.update({n: torch.empty((S * (heads if n == "lse" else 1),), **f32) for n in STATS})
+        self.T = [None] * self.N
         self.grads = {n: torch.zeros(tuple(params[n].shape), **f32) for n in PARAM_NAMES}
         self.launches = 0
         self.events = {"fwd": [], "bwd": []}
         self.gemm_events = None  # list: (start, end, FLOPs) of every GEMM call (bench instrumentation)
+        self.attn_events = None  # list: (start, end) of every attention call
         self._host = {}
 
     # ------------------------------------------------------------------ helpers
     def rows(self, t, i):
         c = self.L.offsets
         return t[c[i]:c[i + 1]]
+
+    def _t1_shape(self, name, s):
+        if name in ("u", "g"):
+            return (s, 4 * self.H), torch.bfloat16
+        if name in TYPE1:
+            return (s, self.H), torch.bfloat16
+        return ((s * self.heads,) if name == "lse" else (s,)), torch.float32
+
+    def _t1_set(self, i):
+        """Chunk i's Type-1 set: row views of the whole-sequence buffers, or fresh allocations."""
+        s = self.L.chunk_len(i)
+        if not self.pool:
+            c = self.L.offsets
+            return {n: (t[c[i] * self.heads:c[i + 1] * self.heads] if n == "lse" else self.rows(t, i))
+                    for n, t in self._full.items()}
+        out = {}
+        for n in TYPE1 + STATS:
+            shape, dt = self._t1_shape(n, s)
+            out[n] = torch.empty(shape, dtype=dt, device=self.device)
+        return out
 
     def _gemm(self, M, N, K, *args, **kw):
         ev = self.gemm_events
@@ -101,6 +131,14 @@ class ChunkedLayer:
             e1.record(kw["stream"])
             ev.append((e0, e1, 2 * M * N * K))
         self.launches += 1
+
+    def _attn_ev(self, strm):
+        if self.attn_events is None:
+            return None
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(strm)
+        self.attn_events.append((e0, e1))
+        return e1
 
     def _ev(self, kind, stream):
         if not self.timing:
@@ -114,24 +152,31 @@ class ChunkedLayer:
         """Per-chunk durations (ms) of the recorded fwd / bwd calls, in call order."""
         return [a.elapsed_time(b) for a, b in self.events[kind]]
 
+    def _kv(self, i):
+        ids = list(range(i + 1))
+        return ids, [self.rows(self.k, j) for j in ids], [self.rows(self.v, j) for j in ids]
+
     # ------------------------------------------------------------------ forward of chunk i
     def forward_chunk(self, i, x, strm):
         p, H, s = self.p, self.H, self.L.chunk_len(i)
         end = self._ev("fwd", strm)
-        r = lambda t: self.rows(t, i)  # noqa: E731
-        self.ctx.layernorm_fwd(r(x), p["ln1_g"], p["ln1_b"], r(self.a), r(self.mu1), r(self.rstd1), eps=LN_EPS,
+        T = self.T[i] = self._t1_set(i)
+        xi = self.rows(x, i)
+        self.ctx.layernorm_fwd(xi, p["ln1_g"], p["ln1_b"], T["a"], T["mu1"], T["rstd1"], eps=LN_EPS, stream=strm)
+        self._gemm(s, 3 * H, H, T["a"], p["w_qkv"], [T["q"], self.rows(self.k, i), self.rows(self.v, i)],
+                   bias=p["b_qkv"], stream=strm)
+        ids, ks, vs = self._kv(i)
+        ae = self._attn_ev(strm)
+        self.ctx.attn_fwd(self.L, i, T["q"], ids, ks, vs, o=T["o"], lse=T["lse"], stream=strm)
+        if ae is not None:
+            ae.record(strm)
+        self._gemm(s, H, H, T["o"], p["w_o"], T["y"], bias=p["b_o"], residual=xi, stream=strm)
+        self.ctx.layernorm_fwd(T["y"], p["ln2_g"], p["ln2_b"], T["b"], T["mu2"], T["rstd2"], eps=LN_EPS,
                                stream=strm)
-        self._gemm(s, 3 * H, H, r(self.a), p["w_qkv"], [r(self.q), r(self.k), r(self.v)], bias=p["b_qkv"],
-                   stream=strm)
-        S = self.S
-        self.att.forward_chunk(i, self.q.view(S, self.heads, self.d), self.k.view(S, self.heads, self.d),
-                               self.v.view(S, self.heads, self.d), strm)
-        self._gemm(s, H, H, r(self.o), p["w_o"], r(self.y), bias=p["b_o"], residual=r(x), stream=strm)
-        self.ctx.layernorm_fwd(r(self.y), p["ln2_g"], p["ln2_b"], r(self.b), r(self.mu2), r(self.rstd2),
-                               eps=LN_EPS, stream=strm)
-        self._gemm(s, 4 * H, H, r(self.b), p["w_1"], r(self.g), bias=p["b_1"], aux_out=r(self.u),
+        self._gemm(s, 4 * H, H, T["b"], p["w_1"], T["g"], bias=p["b_1"], aux_out=T["u"],
                    epilogue=sppo.SPPO_EPI_GELU, stream=strm)
-        self._gemm(s, H, 4 * H, r(self.g), p["w_2"], r(self.z), bias=p["b_2"], residual=r(self.y), stream=strm)
+        self._gemm(s, H, 4 * H, T["g"], p["w_2"], self.rows(self.z, i), bias=p["b_2"], residual=T["y"],
+                   stream=strm)
         self.launches += 3
         if end is not None:
             end.record(strm)
@@ -140,51 +185,57 @@ class ChunkedLayer:
     def backward_chunk(self, i, x, dz, strm):
         p, gr, H, s = self.p, self.grads, self.H, self.L.chunk_len(i)
         end = self._ev("bwd", strm)
-        r = lambda t: self.rows(t, i)  # noqa: E731
+        T = self.T[i]
         ctx = self.ctx
-        du, dbn, dy, da = self.du[:s], self.dbn[:s], self.dy[:s], self.da[:s]
-        dzi = r(dz)
+        du, dbn, dy, da, d_o = self.du[:s], self.dbn[:s], self.dy[:s], self.da[:s], self.d_o[:s]
+        dq, dk, dv = self.dq[:s], self.dkc[:s], self.dvc[:s]
+        dzi, xi = self.rows(dz, i), self.rows(x, i)
         acc = sppo.SPPO_EPI_ACC_F32
         # MLP: fc2 then fc1
-        self._gemm(s, 4 * H, H, dzi, p["w_2"], du, b_mn=1, aux_in=r(self.u), epilogue=sppo.SPPO_EPI_DGELU,
-                   stream=strm)
-        self._gemm(H, 4 * H, s, dzi, r(self.g), gr["w_2"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
+        self._gemm(s, 4 * H, H, dzi, p["w_2"], du, b_mn=1, aux_in=T["u"], epilogue=sppo.SPPO_EPI_DGELU, stream=strm)
+        self._gemm(H, 4 * H, s, dzi, T["g"], gr["w_2"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
         ctx.col_reduce(dzi, s, H, gr["b_2"], stream=strm)
         self._gemm(s, H, 4 * H, du, p["w_1"], dbn, b_mn=1, stream=strm)
-        self._gemm(4 * H, H, s, du, r(self.b), gr["w_1"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
+        self._gemm(4 * H, H, s, du, T["b"], gr["w_1"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
         ctx.col_reduce(du, s, 4 * H, gr["b_1"], stream=strm)
         # LN2 (+ residual stream gradient dz)
-        ctx.layernorm_bwd(dbn, r(self.y), p["ln2_g"], r(self.mu2), r(self.rstd2), dy, dres=dzi, stream=strm)
-        ctx.col_reduce(dbn, s, H, gr["ln2_b"], x=r(self.y), mean=r(self.mu2), rstd=r(self.rstd2),
-                       prod_acc=gr["ln2_g"], stream=strm)
+        ctx.layernorm_bwd(dbn, T["y"], p["ln2_g"], T["mu2"], T["rstd2"], dy, dres=dzi, stream=strm)
+        ctx.col_reduce(dbn, s, H, gr["ln2_b"], x=T["y"], mean=T["mu2"], rstd=T["rstd2"], prod_acc=gr["ln2_g"],
+                       stream=strm)
         # out-proj
-        self._gemm(s, H, H, dy, p["w_o"], r(self.d_o), b_mn=1, stream=strm)
-        self._gemm(H, H, s, dy, r(self.o), gr["w_o"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
+        self._gemm(s, H, H, dy, p["w_o"], d_o, b_mn=1, stream=strm)
+        self._gemm(H, H, s, dy, T["o"], gr["w_o"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
         ctx.col_reduce(dy, s, H, gr["b_o"], stream=strm)
         # attention of chunk i against K/V of chunks 0..i; dK_i, dV_i final afterwards (L11)
-        S, hd = self.S, (self.S, self.heads, self.d)
-        self.att.backward_chunk(i, self.q.view(*hd), self.k.view(*hd), self.v.view(*hd), self.d_o.view(*hd), strm)
-        dq, dk, dv = (r(t.view(S, H)) for t in (self.att.dq, self.att.dk, self.att.dv))
+        ids, ks, vs = self._kv(i)
+        ae = self._attn_ev(strm)
+        ctx.attn_bwd(self.L, i, T["q"], ids, ks, vs, T["o"], T["lse"], d_o, self.delta[:s * self.heads],
+                     self.dq_acc[:s], [self.rows(self.dk_acc, j) for j in ids],
+                     [self.rows(self.dv_acc, j) for j in ids], dq=dq, dk=dk, dv=dv, stream=strm)
+        if ae is not None:
+            ae.record(strm)
         # QKV projection from the three gradient parts, then LN1 (+ dy)
         self._gemm(s, H, 3 * H, [dq, dk, dv], p["w_qkv"], da, b_mn=1, stream=strm)
-        self._gemm(3 * H, H, s, [dq, dk, dv], r(self.a), gr["w_qkv"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
+        self._gemm(3 * H, H, s, [dq, dk, dv], T["a"], gr["w_qkv"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
         ctx.col_reduce([dq, dk, dv], s, 3 * H, gr["b_qkv"], stream=strm)
-        ctx.layernorm_bwd(da, r(x), p["ln1_g"], r(self.mu1), r(self.rstd1), r(self.dx), dres=dy, stream=strm)
-        ctx.col_reduce(da, s, H, gr["ln1_b"], x=r(x), mean=r(self.mu1), rstd=r(self.rstd1), prod_acc=gr["ln1_g"],
+        ctx.layernorm_bwd(da, xi, p["ln1_g"], T["mu1"], T["rstd1"], self.rows(self.dx, i), dres=dy, stream=strm)
+        ctx.col_reduce(da, s, H, gr["ln1_b"], x=xi, mean=T["mu1"], rstd=T["rstd1"], prod_acc=gr["ln1_g"],
                        stream=strm)
-        self.launches += 8
+        self.launches += 3 + 8  # attention bwd (Delta preprocess, main, dQ cast) + LN / column reductions
+        if self.pool:
+            self.T[i] = None  # released: later allocations on this stream are ordered after these kernels
         if end is not None:
             end.record(strm)
 
     def _zero(self):
         for t in self.grads.values():
             t.zero_()
-        self.att.dk_acc.zero_()
-        self.att.dv_acc.zero_()
+        self.dk_acc.zero_()
+        self.dv_acc.zero_()
 
-    # ------------------------------------------------------------------ one step, resident
+    # ------------------------------------------------------------------ one step, no offload
     def step(self, x, dz, stream=None, mark=None):
-        """Forward over chunks 0..N-1 then backward over N-1..0, all resident."""
+        """Forward over chunks 0..N-1 then backward over N-1..0, nothing offloaded."""
         strm = stream or torch.cuda.current_stream()
         self._zero()
         for i in range(self.N):
@@ -196,16 +247,17 @@ class ChunkedLayer:
         return dict(z=self.z, dx=self.dx, grads=self.grads)
 
     # ------------------------------------------------------------------ Type-1 offload with alpha
-    def type1_tensors(self, i):
-        """(name, chunk view, alpha applies) of chunk i's Type-1 tensors."""
-        out = [(n, self.rows(getattr(self, n), i), True) for n in TYPE1]
-        out.append(("lse", self.att.lse_view(i), False))
-        out += [(n, self.rows(getattr(self, n), i), False) for n in STATS]
-        return out
-
     def type1_bytes(self, i):
-        """A_i: bytes of chunk i's Type-1 tensors."""
-        return sum(t.numel() * t.element_size() for _, t, _ in self.type1_tensors(i))
+        """A_i: bytes of chunk i's Type-1 tensors (P:356)."""
+        s = self.L.chunk_len(i)
+        tot = 0
+        for n in TYPE1 + STATS:
+            shape, dt = self._t1_shape(n, s)
+            numel = 1
+            for e in shape:
+                numel *= e
+            tot += numel * (2 if dt == torch.bfloat16 else 4)
+        return tot
 
     def _host_buf(self, key, nbytes):
         if key not in self._host:
@@ -219,32 +271,55 @@ class ChunkedLayer:
 
     def step_offload(self, x, dz, alpha, stream=None, depth: int = 2, poison: bool = False, mark=None):
         """Forward + backward with the alpha_i-prefix of every Type-1 tensor of
-        chunk i offloaded after fwd(i) and prefetched before bwd(i).  With
-        ``poison`` the offloaded device bytes are overwritten (NaN pattern) once
-        the D2H completes, proving the backward reads the prefetched bytes.
-        Returns bytes moved per direction."""
+        chunk i offloaded after fwd(i) and prefetched before bwd(i).  pool mode:
+        the offloaded device memory is released once its D2H completes (see the
+        module docstring).  ``poison`` (resident mode): the offloaded device bytes
+        are overwritten once the D2H completes, proving the backward reads the
+        prefetched bytes.  Returns bytes moved per direction."""
         strm = stream or torch.cuda.current_stream()
         self._zero()
         moved = {"d2h": 0, "h2d": 0}
         plan, done = {}, {}
+        pending = []  # (event, tensors) released once the event has completed (pool)
+
+        def reap(block=False):
+            keep = []
+            for ev, ts in pending:
+                if block:
+                    ev.synchronize()
+                if not (block or ev.query()):
+                    keep.append((ev, ts))
+            pending[:] = keep
+
         for i in range(self.N):
             self.forward_chunk(i, x, strm)
             a = float(alpha[i])
             if a <= 0.0:
                 continue
-            parts = []
-            for name, t, scaled in self.type1_tensors(i):
+            parts = {}
+            T = self.T[i]
+            for name in TYPE1 + STATS:
+                t = T[name]
                 nb = t.numel() * t.element_size()
                 host = self._host_buf((name, i), nb)
                 ev = torch.cuda.Event()
-                n = self.ctx.kv_offload(i, t, host, nb, alpha=(a if scaled else 1.0), producer=strm, done=ev)
+                n = self.ctx.kv_offload(i, t, host, nb, alpha=(a if name in TYPE1 else 1.0), producer=strm, done=ev)
                 moved["d2h"] += n
-                parts.append((t, host, n, ev))
-            plan[i] = parts
-            if poison:
-                for t, _, n, ev in parts:
+                suffix = None
+                if self.pool:
+                    if n < nb:  # keep the resident suffix compactly (device copy, ordered after fwd(i))
+                        suffix = t.reshape(-1).view(torch.uint8)[n:].clone()
+                    pending.append((ev, t))
+                    T[name] = None
+                elif poison:
                     strm.wait_event(ev)
                     t.reshape(-1).view(torch.uint8)[:n].fill_(0xFF)
+                parts[name] = (host, n, nb, suffix, ev)
+            plan[i] = parts
+            if self.pool:
+                self.T[i] = None
+                del T, t
+                reap()
         if mark is not None:
             mark.record(strm)
         issued = set()
@@ -253,14 +328,22 @@ class ChunkedLayer:
             if i < 0 or i in issued or i not in plan:
                 return
             issued.add(i)
+            T = self._t1_set(i) if self.pool else self.T[i]
             evs = []
-            for t, host, n, ev in plan[i]:
+            for name, (host, n, nb, suffix, ev) in plan[i].items():
+                t = T[name]
                 strm.wait_event(ev)  # the bytes reached the host (its D2H completed)
                 pe = torch.cuda.Event()
+                # ordered after the work already on strm (the fresh allocation's previous users)
                 self.ctx.kv_prefetch(i, host, t, n, consumer=strm, done=pe, flags=sppo.SPPO_COPY_DEFER_WAIT)
                 moved["h2d"] += n
+                if suffix is not None:
+                    t.reshape(-1).view(torch.uint8)[n:].copy_(suffix)
                 evs.append(pe)
+            if self.pool:
+                self.T[i] = T
             done[i] = evs
+            plan[i] = {}  # drop the suffix copies (released after the restores enqueued above)
 
         for i in range(self.N - 1, -1, -1):
             for dd in range(depth):
@@ -268,6 +351,9 @@ class ChunkedLayer:
             for pe in done.get(i, []):
                 strm.wait_event(pe)
             self.backward_chunk(i, x, dz, strm)
+            if self.pool:
+                reap()
+        reap(block=True)
         return moved
 
     def alpha_plan(self, fwd_ms, bw_d2h_gbs):

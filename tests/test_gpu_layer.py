@@ -125,3 +125,45 @@ def test_layer_type1_offload_poisoned_equals_resident(ctx):
         rel = (got.double() - ref[k].double()).norm() / ref[k].double().norm()
         assert rel < 1e-5, (k, float(rel))
     lay.free_host()
+
+
+@pytest.mark.parametrize("alpha", [[1.0, 1.0, 1.0, 0.0], [0.3, 0.7, 1.0, 0.0], [0.0, 0.5, 0.0, 0.0]])
+def test_layer_pool_offload_equals_resident_and_frees_memory(ctx, alpha):
+    """pool mode: chunk activation sets are separate allocations released after
+    their D2H (suffix 1 - alpha kept compactly) and rebuilt before bwd(i).
+    Results equal the resident step (forward bitwise, gradients to fp32 atomics
+    order); the peak device memory of the offloaded step is below the
+    all-resident step's when every chunk but the last is fully offloaded."""
+    from paper_2503_10377_b200 import engine_layer, sppo
+    S, H, heads = 2048, 512, 4
+    params, io = _setup(S, H, 6)
+    dev = {k: v.cuda() for k, v in params.items()}
+    off = sppo.partition_equal(S, 4)
+    x, dz = io["x"].cuda(), io["dz"].cuda()
+    ref_lay = engine_layer.ChunkedLayer(ctx, H, heads, off, dev)
+    r = ref_lay.step(x, dz)
+    ref = {"z": r["z"].clone(), "dx": r["dx"].clone(), **{k: v.clone() for k, v in r["grads"].items()}}
+    del ref_lay, r
+    torch.cuda.synchronize()
+    lay = engine_layer.ChunkedLayer(ctx, H, heads, off, dev, pool=True)
+    lay.step(x, dz)  # warm the caching allocator
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    lay.step(x, dz)
+    torch.cuda.synchronize()
+    peak_resident = torch.cuda.max_memory_allocated() - base
+    torch.cuda.reset_peak_memory_stats()
+    moved = lay.step_offload(x, dz, alpha)
+    torch.cuda.synchronize()
+    peak_offload = torch.cuda.max_memory_allocated() - base
+    assert moved["d2h"] == moved["h2d"] > 0
+    assert torch.equal(lay.z, ref["z"])
+    for k in ["dx"] + list(L.PARAM_NAMES):
+        got = lay.dx if k == "dx" else lay.grads[k]
+        rel = (got.double() - ref[k].double()).norm() / ref[k].double().norm()
+        assert rel < 1e-5, (k, float(rel))
+    if alpha[0] == 1.0:
+        a1 = lay.type1_bytes(0)
+        assert peak_offload < peak_resident - a1, (peak_offload, peak_resident, a1)
+    lay.free_host()
