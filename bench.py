@@ -684,6 +684,123 @@ def run_layer(args, cfg, ws, rank, local):
     return line if rank == 0 else None
 
 
+def run_layer_pool(args, cfg, ws, rank, local):
+    """The layer step with two-level activation management that actually frees
+    memory (engine_layer pool mode): every chunk's Type-1 set leaves the GPU as
+    its alpha-prefix after fwd(i) and is rebuilt before bwd(i).  Needed where the
+    all-resident step does not fit (e.g. C3's 1M tokens at hidden 4096).  Warm-up
+    steps 1-2 run alpha = 1, step 2 measures the per-chunk forward times; alpha is then
+    the sequence-aware plan.  value = FLOPs / offloaded step time."""
+    from paper_2503_10377_b200 import engine_layer, sppo
+    import synth
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    heads, d, S, N = cfg["heads"], cfg["d"], cfg["S"], cfg["N"]
+    H = heads * d
+    ctx = sppo.Context(local)
+    offsets = sppo.partition_balanced(S, N) if args.partition == "balanced" else sppo.partition_equal(S, N)
+    params = synth.make_layer_params(H, 0, device=dev)
+    io = synth.make_layer_io(S, H, 0, device=dev)
+    lay = engine_layer.ChunkedLayer(ctx, H, heads, offsets, params, device=dev, pool=True)
+    stream = torch.cuda.current_stream()
+    bw = 56.0  # GB/s pinned D2H measured on this pool (profiles/r01/box_probe.json)
+    full = [1.0] * (N - 1) + [0.0]
+    lay.step_offload(io["x"], io["dz"], full, stream)  # warm-up (allocator, pinned host buffers)
+    lay.timing = True
+    lay.events = {"fwd": [], "bwd": []}
+    lay.step_offload(io["x"], io["dz"], full, stream)
+    torch.cuda.synchronize()
+    t_fwd = lay.chunk_ms("fwd")
+    lay.timing = False
+    alpha = lay.alpha_plan(t_fwd, bw)
+    for _ in range(max(0, args.warmup - 2)):
+        lay.step_offload(io["x"], io["dz"], alpha, stream)
+    torch.cuda.synchronize()
+    lay.launches = 0
+    torch.cuda.reset_peak_memory_stats(dev)
+    barrier(ws)
+    clk = ClockSampler(local)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    phase = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    moved = None
+    for st in range(args.steps):
+        marks[st].record(stream)
+        moved = lay.step_offload(io["x"], io["dz"], alpha, stream, mark=phase[st])
+    marks[args.steps].record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    launches = lay.launches // args.steps
+    peak = torch.cuda.max_memory_allocated(dev)
+    barrier(ws)
+    ms = max_over_ranks(marks[0].elapsed_time(marks[args.steps]) / args.steps, ws)
+    fwd_ms = sum(marks[i].elapsed_time(phase[i]) for i in range(args.steps)) / args.steps
+    bwd_ms = sum(phase[i].elapsed_time(marks[i + 1]) for i in range(args.steps)) / args.steps
+    pairs = sppo.causal_pairs(offsets)
+    f_gemm_fwd, f_attn_fwd = 24 * H * H * S, 4 * d * heads * pairs
+    f_fwd = f_gemm_fwd + f_attn_fwd
+    f_bwd = 2 * f_gemm_fwd + 10 * d * heads * pairs
+    fl = f_fwd + f_bwd
+    peaks = load_peaks()
+    tflops = fl / (ms * 1e-3) / 1e12
+    # one instrumented step: GEMM / attention device time
+    lay.gemm_events, lay.attn_events = [], []
+    lay.step_offload(io["x"], io["dz"], alpha, stream)
+    torch.cuda.synchronize()
+    gemm_ms = sum(a.elapsed_time(b) for a, b, _ in lay.gemm_events)
+    gemm_fl = sum(f for _, _, f in lay.gemm_events)
+    attn_ms = sum(a.elapsed_time(b) for a, b in lay.attn_events)
+    lay.gemm_events = lay.attn_events = None
+    # the paper's fixed alpha = 1 (every chunk's activations fully offloaded) for comparison
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    fix_moved = lay.step_offload(io["x"], io["dz"], full, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    fix_ms = e0.elapsed_time(e1)
+    lay.free_host()
+    A = [lay.type1_bytes(i) for i in range(N)]
+    total_mem = torch.cuda.get_device_properties(dev).total_memory
+    # device bytes an all-resident step would need on top of what this one keeps: every
+    # chunk's Type-1 set at once (the pool step keeps only suffixes + in-flight sets)
+    resident_need = peak + sum(A) - max(A) * 3
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        c = cpu_oracle_layer_sample(H, heads)
+        cpu = {"value": round(c["value"], 6), "unit": "TFLOP/s", "cores": c["cores"], "kind": "oracle",
+               "sample": c["sample"]}
+    gemm_tf = gemm_fl / (gemm_ms * 1e-3) / 1e12
+    line = {"metric": LAYER_METRIC, "value": round(tflops * ws, 2), "unit": "TFLOP/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": cfg["workload"].replace("shape", "layer") + " -- full GPT layer (hidden "
+                                   f"{H}) per chunk, Type-1 activations offloaded (pool: device copies freed)",
+                       "hidden": H, "heads": heads, "seq_len": S, "chunks": N, "partition": args.partition,
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "l2": "inputs larger than L2"},
+            "tokens_per_s": round(S * ws / (ms * 1e-3), 1), "pct_of_bf16_peak": round(100 * tflops / peaks["burst"], 2),
+            "fwd_tflops": round(f_fwd / (fwd_ms * 1e-3) / 1e12, 1), "bwd_tflops": round(f_bwd / (bwd_ms * 1e-3) / 1e12, 1),
+            "breakdown": {"gemm_ms": round(gemm_ms, 3), "gemm_tflops": round(gemm_tf, 1),
+                          "attention_ms": round(attn_ms, 3),
+                          "attention_tflops": round((f_attn_fwd * 3.5) / (attn_ms * 1e-3) / 1e12, 1)},
+            "memory": {"peak_allocated_gb": round(peak / 1e9, 2), "device_total_gb": round(total_mem / 1e9, 2),
+                       "type1_bytes_all_chunks_gb": round(sum(A) / 1e9, 2),
+                       "all_resident_estimate_gb": round(resident_need / 1e9, 2),
+                       "fits_without_offload": bool(resident_need < total_mem)},
+            "offload": {"alpha": [round(a, 3) for a in alpha], "d2h_bytes": moved["d2h"], "h2d_bytes": moved["h2d"],
+                        "fixed_alpha1": {"ms": round(fix_ms, 3), "slowdown_pct": round(100 * (fix_ms - ms) / ms, 2),
+                                         "d2h_bytes": fix_moved["d2h"]},
+                        "fwd_ms_per_chunk_calibration": [round(t, 3) for t in t_fwd], "bw_d2h_gbs_assumed": bw},
+            "gpu_launches": launches,
+            "roofline": {"bound": "tensor", "kernel": "gemm_kernel (all layer GEMMs, event-timed in one step)",
+                         "achieved": round(gemm_tf, 1), "peak": peaks["burst"], "unit": "TFLOP/s",
+                         "frac": round(gemm_tf / peaks["burst"], 3), "traffic": None,
+                         "peak_source": peaks["source"] + " bf16 burst"},
+            "clocks": clocks, "e2e": None, "cpu_baseline": cpu}
+    ctx.close()
+    return line if rank == 0 else None
+
+
 # ------------------------------------------------------------------ reference arm (the oracle)
 def run_reference(args, cfg, ws, rank):
     if rank != 0:
@@ -723,6 +840,8 @@ def main():
                     help="GB of device memory for the step: picks the KV hot prefix that fits (0: off)")
     ap.add_argument("--partition", default="equal", choices=["equal", "balanced"])
     ap.add_argument("--shard-of", type=int, default=1, help="1 GPU: run rank 0's heads of a G-GPU split")
+    ap.add_argument("--layer-pool", action="store_true",
+                    help="layer workload with activation sets freed after offload (fits C3's 1M tokens)")
     ap.add_argument("--workload", default="attention", choices=["attention", "layer"],
                     help="attention: the chunked attention hot path (headline); layer: full GPT layer per chunk")
     ap.add_argument("--parallel", default="heads", choices=["heads", "cp"],
@@ -735,7 +854,7 @@ def main():
     if args.impl == "reference":
         line = run_reference(args, cfg, ws, rank)
     elif args.workload == "layer":
-        line = run_layer(args, cfg, ws, rank, local)
+        line = (run_layer_pool if args.layer_pool else run_layer)(args, cfg, ws, rank, local)
     elif args.parallel == "cp":
         line = run_cp(args, cfg, ws, rank, local)
     else:

@@ -280,16 +280,16 @@ class ChunkedLayer:
         self._zero()
         moved = {"d2h": 0, "h2d": 0}
         plan, done = {}, {}
-        pending = []  # (event, tensors) released once the event has completed (pool)
+        # pool: per offloaded chunk, (its last D2H event, its device tensors).  The
+        # host enqueues far ahead of the GPU, so completed copies cannot be found by
+        # polling alone: with more than `inflight` chunks pending the host waits for
+        # the oldest one's D2H (the GPU still has the chunks enqueued since then).
+        pending = []
 
-        def reap(block=False):
-            keep = []
-            for ev, ts in pending:
-                if block:
-                    ev.synchronize()
-                if not (block or ev.query()):
-                    keep.append((ev, ts))
-            pending[:] = keep
+        def reap(block=False, inflight=2):
+            while pending and (block or len(pending) > inflight or pending[0][0].query()):
+                pending[0][0].synchronize()
+                pending.pop(0)
 
         for i in range(self.N):
             self.forward_chunk(i, x, strm)
@@ -297,6 +297,7 @@ class ChunkedLayer:
             if a <= 0.0:
                 continue
             parts = {}
+            held = []
             T = self.T[i]
             for name in TYPE1 + STATS:
                 t = T[name]
@@ -309,7 +310,7 @@ class ChunkedLayer:
                 if self.pool:
                     if n < nb:  # keep the resident suffix compactly (device copy, ordered after fwd(i))
                         suffix = t.reshape(-1).view(torch.uint8)[n:].clone()
-                    pending.append((ev, t))
+                    held.append(t)
                     T[name] = None
                 elif poison:
                     strm.wait_event(ev)
@@ -318,7 +319,8 @@ class ChunkedLayer:
             plan[i] = parts
             if self.pool:
                 self.T[i] = None
-                del T, t
+                pending.append((ev, held))  # ev: this chunk's last D2H (the D2H stream is in order)
+                del T, t, held
                 reap()
         if mark is not None:
             mark.record(strm)
