@@ -514,6 +514,17 @@ def cpu_oracle_layer_sample(H, heads):
                 sample=f"oracle fp64 layer fwd+bwd, {S_s} tokens (2 chunks), H={H}, {fl:.3e} FLOP in {dt:.1f}s")
 
 
+def layer_offsets(args, S, N, H):
+    """a0 for the layer: equal, attention-balanced (pairs only) or layer-balanced
+    (pairs + the token-wise GEMM work: 72 h^2 s + 14 h pairs FLOPs -> lin = 36 h / 7)."""
+    from paper_2503_10377_b200 import sppo
+    if args.partition == "balanced":
+        return sppo.partition_balanced(S, N)
+    if args.partition == "layer-balanced":
+        return sppo.partition_balanced(S, N, 36 * H // 7)
+    return sppo.partition_equal(S, N)
+
+
 def run_layer(args, cfg, ws, rank, local):
     """One step = the GPT layer (hidden = heads*d of the config) forward over the
     N chunks then backward in reverse (engine_layer.ChunkedLayer).  N > 1 ranks
@@ -527,7 +538,7 @@ def run_layer(args, cfg, ws, rank, local):
     heads, d, S, N = cfg["heads"], cfg["d"], cfg["S"], cfg["N"]
     H = heads * d
     ctx = sppo.Context(local)
-    offsets = sppo.partition_balanced(S, N) if args.partition == "balanced" else sppo.partition_equal(S, N)
+    offsets = layer_offsets(args, S, N, H)
     params = synth.make_layer_params(H, 0, device=dev)
     io = synth.make_layer_io(S, H, 0, device=dev)
     lay = engine_layer.ChunkedLayer(ctx, H, heads, offsets, params, device=dev)
@@ -699,7 +710,7 @@ def run_layer_pool(args, cfg, ws, rank, local):
     heads, d, S, N = cfg["heads"], cfg["d"], cfg["S"], cfg["N"]
     H = heads * d
     ctx = sppo.Context(local)
-    offsets = sppo.partition_balanced(S, N) if args.partition == "balanced" else sppo.partition_equal(S, N)
+    offsets = layer_offsets(args, S, N, H)
     params = synth.make_layer_params(H, 0, device=dev)
     io = synth.make_layer_io(S, H, 0, device=dev)
     lay = engine_layer.ChunkedLayer(ctx, H, heads, offsets, params, device=dev, pool=True)
@@ -838,7 +849,7 @@ def main():
                     help="resident step: forward launches alternate over this many streams (default: by launch size)")
     ap.add_argument("--device-budget", type=float, default=0.0,
                     help="GB of device memory for the step: picks the KV hot prefix that fits (0: off)")
-    ap.add_argument("--partition", default="equal", choices=["equal", "balanced"])
+    ap.add_argument("--partition", default="equal", choices=["equal", "balanced", "layer-balanced"])
     ap.add_argument("--shard-of", type=int, default=1, help="1 GPU: run rank 0's heads of a G-GPU split")
     ap.add_argument("--layer-pool", action="store_true",
                     help="layer workload with activation sets freed after offload (fits C3's 1M tokens)")

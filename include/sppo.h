@@ -223,6 +223,11 @@ sppo_status sppo_partition_equal(int64_t S, int32_t N, int64_t* offsets_out);
  * ties broken toward longer leading chunks (lengths come out non-increasing).
  * Writes N+1 offsets.  O(N log^2 S). */
 sppo_status sppo_partition_balanced(int64_t S, int32_t N, int64_t* offsets_out);
+/* Same with a per-token linear term (S:46 [forward_flops] c_lin H^2 s_len; the
+ * token-wise GEMM / LayerNorm work of a full layer): minimises
+ * max_i (pairs_i + lin * s_i), lin in pair units (e.g. a GPT layer, fwd+bwd:
+ * 72 h^2 s + 14 h pairs FLOPs -> lin = 36 h / 7).  lin = 0 is the call above. */
+sppo_status sppo_partition_balanced_lin(int64_t S, int32_t N, int64_t lin, int64_t* offsets_out);
 /* Causal (q,k) pairs of all chunks: sum_i s_i c_i + s_i (s_i + 1) / 2. */
 sppo_status sppo_causal_pairs(const int64_t* offsets, int32_t N, int64_t* pairs_out);
 /* Sequence-aware offload ratio (P:371-377 [§5.2]; reading L9):

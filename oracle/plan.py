@@ -47,16 +47,18 @@ def partition_equal(S: int, N: int):
     return [base + (1 if i < rem else 0) for i in range(N)]
 
 
-def partition_min_max_pairs(S: int, N: int):
+def partition_min_max_pairs(S: int, N: int, lin: int = 0):
     """FLOPs-balanced partition (P:253, P:256, P:327 [§3.2, §4]):
     the N chunk lengths minimising max_i causal_pairs(s_i, c_i), by exact dynamic
     programming over split points (small S only).  Among optimal partitions the
     lexicographically largest length vector is returned ("ties broken toward the
     longer first chunk").  Cost of a chunk [a, b) is T(b) - T(a) with
-    T(x) = x (x + 1) / 2 (the causal pairs of rows a..b-1)."""
+    T(x) = x (x + 1) / 2 (the causal pairs of rows a..b-1), plus lin (b - a) for a
+    per-token linear term (c_lin: the token-wise work of a full layer)."""
     if not (1 <= N <= S):
         raise ValueError("1 <= N <= S required")
-    T = lambda x: x * (x + 1) // 2
+    T0 = lambda x: x * (x + 1) // 2  # noqa: E731
+    T = lambda x: T0(x) + lin * x  # noqa: E731  (cost(a, b) = T(b) - T(a))
     INF = float("inf")
     # best[k][e] = min over partitions of [0, e) into k chunks of the max chunk cost
     best = [[INF] * (S + 1) for _ in range(N + 1)]

@@ -602,12 +602,16 @@ sppo_status sppo_partition_equal(int64_t S, int32_t N, int64_t* out) {
 namespace {
 int64_t tri(int64_t x) { return x * (x + 1) / 2; }  // causal pairs of rows 0..x-1
 
-// Largest b in (a, S] with tri(b) - tri(a) <= B (a itself if none).
-int64_t greedy_end(int64_t a, int64_t S, int64_t B) {
+// cost of chunk [a, b): its causal pairs plus `lin` per token (the token-wise
+// layer work in pair units; 0 = attention only)
+int64_t chunk_cost(int64_t a, int64_t b, int64_t lin) { return tri(b) - tri(a) + lin * (b - a); }
+
+// Largest b in (a, S] with chunk_cost(a, b) <= B (a itself if none).
+int64_t greedy_end(int64_t a, int64_t S, int64_t B, int64_t lin = 0) {
   int64_t lo = a, hi = S;
   while (lo < hi) {
     const int64_t mid = lo + (hi - lo + 1) / 2;
-    if (tri(mid) - tri(a) <= B)
+    if (chunk_cost(a, mid, lin) <= B)
       lo = mid;
     else
       hi = mid - 1;
@@ -616,10 +620,10 @@ int64_t greedy_end(int64_t a, int64_t S, int64_t B) {
 }
 
 // Chunks a greedy cover of [0, S) needs when no chunk may exceed B pairs (INT64_MAX if impossible).
-int64_t chunks_needed(int64_t S, int64_t B) {
+int64_t chunks_needed(int64_t S, int64_t B, int64_t lin = 0) {
   int64_t a = 0, n = 0;
   while (a < S) {
-    const int64_t b = greedy_end(a, S, B);
+    const int64_t b = greedy_end(a, S, B, lin);
     if (b == a) return INT64_MAX;
     a = b;
     ++n;
@@ -628,14 +632,15 @@ int64_t chunks_needed(int64_t S, int64_t B) {
 }
 }  // namespace
 
-sppo_status sppo_partition_balanced(int64_t S, int32_t N, int64_t* out) {
+sppo_status sppo_partition_balanced_lin(int64_t S, int32_t N, int64_t lin, int64_t* out) {
   if (!out) return fail(SPPO_E_ARG, "out is NULL");
   if (N < 1 || S < N || S > (int64_t)INT32_MAX) return fail(SPPO_E_SHAPE, "need 1 <= N <= S < 2^31");
+  if (lin < 0 || lin > ((int64_t)1 << 30)) return fail(SPPO_E_ARG, "lin = %lld not in [0, 2^30]", (long long)lin);
   // smallest achievable max-chunk cost B*: binary search on the greedy cover count
-  int64_t lo = S, hi = tri(S);  // the last row alone costs S pairs
+  int64_t lo = S + lin, hi = chunk_cost(0, S, lin);  // the last row alone costs S + lin
   while (lo < hi) {
     const int64_t mid = lo + (hi - lo) / 2;
-    if (chunks_needed(S, mid) <= N)
+    if (chunks_needed(S, mid, lin) <= N)
       hi = mid;
     else
       lo = mid + 1;
@@ -647,7 +652,7 @@ sppo_status sppo_partition_balanced(int64_t S, int32_t N, int64_t* out) {
   int64_t a = 0;
   for (int32_t i = 0; i < N; ++i) {
     const int64_t remaining = N - i - 1;
-    int64_t b = greedy_end(a, S, B);
+    int64_t b = greedy_end(a, S, B, lin);
     if (b > S - remaining) b = S - remaining;
     if (b <= a) return fail(SPPO_E_SHAPE, "balanced partition failed (S=%lld, N=%d)", (long long)S, N);
     out[i + 1] = b;
@@ -655,6 +660,10 @@ sppo_status sppo_partition_balanced(int64_t S, int32_t N, int64_t* out) {
   }
   if (out[N] != S) return fail(SPPO_E_SHAPE, "balanced partition does not cover S (S=%lld, N=%d)", (long long)S, N);
   return SPPO_OK;
+}
+
+sppo_status sppo_partition_balanced(int64_t S, int32_t N, int64_t* out) {
+  return sppo_partition_balanced_lin(S, N, 0, out);
 }
 
 sppo_status sppo_causal_pairs(const int64_t* off, int32_t N, int64_t* pairs) {

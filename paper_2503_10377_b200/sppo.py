@@ -27,7 +27,8 @@ STATUS = {0: "SPPO_OK", 1: "SPPO_E_ARG", 2: "SPPO_E_SHAPE", 3: "SPPO_E_ALIGN", 4
 # every symbol include/sppo.h declares
 EXPORTS = ("sppo_ctx_create", "sppo_ctx_destroy", "sppo_ctx_sync", "sppo_last_error", "sppo_version",
            "sppo_attn_fwd", "sppo_attn_bwd", "sppo_host_alloc", "sppo_host_free", "sppo_kv_offload",
-           "sppo_kv_prefetch", "sppo_partition_equal", "sppo_partition_balanced", "sppo_causal_pairs", "sppo_offload_alpha",
+           "sppo_kv_prefetch", "sppo_partition_equal", "sppo_partition_balanced", "sppo_partition_balanced_lin", "sppo_causal_pairs",
+           "sppo_offload_alpha",
            "sppo_finalize", "sppo_ctx_streams")
 # every symbol include/sppo_layer.h declares (per-chunk transformer layer)
 LAYER_EXPORTS = ("sppo_gemm", "sppo_layernorm_fwd", "sppo_layernorm_bwd", "sppo_col_reduce")
@@ -91,6 +92,7 @@ def _load():
         "sppo_kv_prefetch": ([vp, i32, vp, vp, sz, vp, vp, i32], i32),
         "sppo_partition_equal": ([C.c_int64, i32, C.POINTER(C.c_int64)], i32),
         "sppo_partition_balanced": ([C.c_int64, i32, C.POINTER(C.c_int64)], i32),
+        "sppo_partition_balanced_lin": ([C.c_int64, i32, C.c_int64, C.POINTER(C.c_int64)], i32),
         "sppo_causal_pairs": ([C.POINTER(C.c_int64), i32, C.POINTER(C.c_int64)], i32),
         "sppo_offload_alpha": ([C.POINTER(C.c_double), C.POINTER(C.c_double), i32, C.c_double,
                                 C.POINTER(C.c_double)], i32),
@@ -161,9 +163,12 @@ def partition_equal(S: int, N: int):
     return list(out)
 
 
-def partition_balanced(S: int, N: int):
+def partition_balanced(S: int, N: int, lin: int = 0):
     out = (C.c_int64 * (N + 1))()
-    _check(_lib.sppo_partition_balanced(S, N, out))
+    if lin:
+        _check(_lib.sppo_partition_balanced_lin(S, N, int(lin), out))
+    else:
+        _check(_lib.sppo_partition_balanced(S, N, out))
     return list(out)
 
 
