@@ -123,9 +123,10 @@ struct GemmParams {
   int32_t c_parts, c_part_w;
   void* c[3];
 };
-// maps: a[0..a_parts-1], b.  bn = 128 | 256.
-cudaError_t launch_gemm_sm100(const void* tmap_a3, const void* tmap_b, const GemmParams& p, int bn, int num_sms,
-                              cudaStream_t s);
+// maps: a[0..a_parts-1], b.  bn = 128 | 256 (single CTA); pair: the cluster-of-2
+// 256 x 256 kernel (b's K-major box then spans 128 rows).
+cudaError_t launch_gemm_sm100(const void* tmap_a3, const void* tmap_b, const GemmParams& p, int bn, bool pair,
+                              int num_sms, cudaStream_t s);
 cudaError_t launch_layernorm_fwd(const void* x, const void* gamma, const void* beta, int64_t rows, int cols,
                                  float eps, void* y, float* mean, float* rstd, cudaStream_t s);
 cudaError_t launch_layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean,

@@ -463,11 +463,11 @@ cudaError_t launch_bn(const CUtensorMap* ta, const CUtensorMap* tb, const GemmPa
 
 }  // namespace
 
-cudaError_t launch_gemm_sm100(const void* tmap_a3, const void* tmap_b, const GemmParams& p, int bn, int num_sms,
-                              cudaStream_t s) {
+cudaError_t launch_gemm_sm100(const void* tmap_a3, const void* tmap_b, const GemmParams& p, int bn, bool pair,
+                              int num_sms, cudaStream_t s) {
   const CUtensorMap* ta = static_cast<const CUtensorMap*>(tmap_a3);
   const CUtensorMap* tb = static_cast<const CUtensorMap*>(tmap_b);
-  if (bn == 2256) return launch_pair(ta, tb, p, num_sms, s);
+  if (pair) return launch_pair(ta, tb, p, num_sms, s);
   return bn == 256 ? launch_bn<256>(ta, tb, p, num_sms, s) : launch_bn<128>(ta, tb, p, num_sms, s);
 }
 

@@ -135,7 +135,7 @@ sppo_status sppo_gemm(sppo_ctx ctx, const sppo_gemm_args* g, void* stream) {
   p.c_parts = g->c_parts;
   p.c_part_w = (int32_t)cpw;
   for (int i = 0; i < 3; ++i) p.c[i] = i < g->c_parts ? g->c[i] : g->c[0];
-  cudaError_t e = launch_gemm_sm100(ta, &tb, p, pair ? 2256 : bn, sm_count(), (cudaStream_t)stream);
+  cudaError_t e = launch_gemm_sm100(ta, &tb, p, bn, pair, sm_count(), (cudaStream_t)stream);
   if (e != cudaSuccess) return err(SPPO_E_CUDA, "gemm launch: %s", cudaGetErrorString(e));
   return SPPO_OK;
 }
