@@ -123,7 +123,9 @@ def test_layer_type1_offload_poisoned_equals_resident(ctx):
     for k in ["dx"] + list(L.PARAM_NAMES):
         got = lay.dx if k == "dx" else lay.grads[k]
         rel = (got.double() - ref[k].double()).norm() / ref[k].double().norm()
-        assert rel < 1e-5, (k, float(rel))
+        # the backward's fp32 reduction order is not fixed (dQ TMA reduce-add, column
+        # atomics), which can flip bf16 roundings of dq / da downstream: 1.2e-5 seen
+        assert rel < 1e-4, (k, float(rel))
     lay.free_host()
 
 
@@ -162,7 +164,9 @@ def test_layer_pool_offload_equals_resident_and_frees_memory(ctx, alpha):
     for k in ["dx"] + list(L.PARAM_NAMES):
         got = lay.dx if k == "dx" else lay.grads[k]
         rel = (got.double() - ref[k].double()).norm() / ref[k].double().norm()
-        assert rel < 1e-5, (k, float(rel))
+        # the backward's fp32 reduction order is not fixed (dQ TMA reduce-add, column
+        # atomics), which can flip bf16 roundings of dq / da downstream: 1.2e-5 seen
+        assert rel < 1e-4, (k, float(rel))
     if alpha[0] == 1.0:
         a1 = lay.type1_bytes(0)
         assert peak_offload < peak_resident - a1, (peak_offload, peak_resident, a1)
