@@ -50,7 +50,10 @@ struct GemmBars {
 // Tile t -> (m block, n block), grouped raster: kGroupM consecutive m blocks sweep
 // the n blocks together, so the CTAs running at one time share a few A row panels
 // and B column panels (L2 reuse) instead of all of A.
-constexpr int kGroupM = 8;
+#ifndef SPPO_GEMM_GROUP
+#define SPPO_GEMM_GROUP 8
+#endif
+constexpr int kGroupM = SPPO_GEMM_GROUP;
 __device__ __forceinline__ void tile_coords(int t, int Mt, int Nt, int& mb, int& nb) {
   const int per_group = kGroupM * Nt;
   const int g = t / per_group, r = t - g * per_group;
@@ -214,6 +217,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== MMA issuer =====================
     const uint32_t idesc = idesc_bf16(BM, BN, p.a_mn, p.b_mn);
     const uint32_t sbase = smem_u32(smem);
+    // base descriptors once; a stage / K=16 step adds (byte offset >> 4) to the
+    // start-address field (smem addresses < 2^18: no carry out of the field)
+    const uint64_t a0 = p.a_mn ? sdesc_mnmajor(sbase, kMnBox) : sdesc_kmajor(sbase);
+    const uint64_t b0 = p.b_mn ? sdesc_mnmajor(sbase + C::kABytes, kMnBox) : sdesc_kmajor(sbase + C::kABytes);
+    const uint32_t a_k = (p.a_mn ? 2048u : 32u) >> 4, b_k = (p.b_mn ? 2048u : 32u) >> 4;
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -225,14 +233,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < Kt; ++kb) {
         mbar_wait(&bars.full[stage], phase);
         tc_fence_after();
-        const uint32_t a_addr = sbase + stage * C::kStageBytes;
-        const uint32_t b_addr = a_addr + C::kABytes;
+        const uint64_t so = (uint64_t)((stage * C::kStageBytes) >> 4);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          const uint64_t ad = p.a_mn ? sdesc_mnmajor(a_addr + k * 2048, kMnBox) : sdesc_kmajor(a_addr + k * 32);
-          const uint64_t bd = p.b_mn ? sdesc_mnmajor(b_addr + k * 2048, kMnBox) : sdesc_kmajor(b_addr + k * 32);
-          mma_ss_w(d, ad, bd, idesc, (kb | k) != 0);
-        }
+        for (int k = 0; k < BK / 16; ++k)
+          mma_ss_w(d, a0 + so + k * a_k, b0 + so + k * b_k, idesc, (kb | k) != 0);
         mma_commit_w(&bars.empty[stage]);
         if (++stage == C::kStages) {
           stage = 0;
@@ -368,6 +372,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (leader) {
       const uint32_t idesc = idesc_bf16(256, 256, p.a_mn, p.b_mn);
       const uint32_t sbase = smem_u32(smem);
+      const uint64_t a0 = p.a_mn ? sdesc_mnmajor(sbase, kMnBox) : sdesc_kmajor(sbase);
+      const uint64_t b0 = p.b_mn ? sdesc_mnmajor(sbase + kPairA, kMnBox) : sdesc_kmajor(sbase + kPairA);
+      const uint32_t a_k = (p.a_mn ? 2048u : 32u) >> 4, b_k = (p.b_mn ? 2048u : 32u) >> 4;
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -379,14 +386,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < Kt; ++kb) {
           mbar_wait(&bars.full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = sbase + stage * kPairStage;
-          const uint32_t b_addr = a_addr + kPairA;
+          const uint64_t so = (uint64_t)((stage * kPairStage) >> 4);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = p.a_mn ? sdesc_mnmajor(a_addr + k * 2048, kMnBox) : sdesc_kmajor(a_addr + k * 32);
-            const uint64_t bd = p.b_mn ? sdesc_mnmajor(b_addr + k * 2048, kMnBox) : sdesc_kmajor(b_addr + k * 32);
-            mma2_ss_w(d, ad, bd, idesc, (kb | k) != 0);
-          }
+          for (int k = 0; k < BK / 16; ++k)
+            mma2_ss_w(d, a0 + so + k * a_k, b0 + so + k * b_k, idesc, (kb | k) != 0);
           mma2_commit_w(&bars.empty[stage]);
           if (++stage == kPairStages) {
             stage = 0;
