@@ -818,13 +818,14 @@ def run_reference(args, cfg, ws, rank):
         return None
     res = []
     c = None
+    layer = args.workload == "layer"
     for it in range(args.warmup + args.steps):
-        c = cpu_oracle_sample()
+        c = cpu_oracle_layer_sample(cfg["heads"] * cfg["d"], cfg["heads"]) if layer else cpu_oracle_sample()
         if it >= args.warmup:
             res.append(c)
     secs = statistics.median([r["seconds"] for r in res])
     val = statistics.median([r["value"] for r in res])
-    return {"metric": METRIC, "value": round(val, 6), "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
+    return {"metric": LAYER_METRIC if layer else METRIC, "value": round(val, 6), "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(secs * 1e3, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": cfg["workload"] + " -- bounded oracle sample per step", "sample": c["sample"]},
