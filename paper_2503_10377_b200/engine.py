@@ -415,6 +415,151 @@ class ChunkedAttention:
                 self._last_off_ev = poison_ev
         return stats
 
+    def step_kv_stream_grouped(self, q, k, v, do, hot: int, window: int, group: int = 2, stream=None,
+                               poison: bool = False):
+        """KV streaming (step_kv_stream's policy, L10) with the cold windows shared
+        by ``group`` consecutive chunks: each streamed window of K_j, V_j is applied
+        to the forwards of chunks i..i+G-1 (each with its own FIRST/LAST carry) or
+        to the backwards of chunks i..i-G+1 (descending, so a chunk's final dK/dV
+        is written after every later chunk's contribution) before the ring slot is
+        refilled — the host->device KV volume drops by ~G.  Chunk j only ever sees
+        ids <= j, so the results equal the ungrouped step up to fp32 accumulation
+        order.  Trade-off: a group's chunks finish together (coarser sequence
+        pipelining granularity).  Returns copy statistics."""
+        L = self.L
+        N = L.num_chunks
+        h, d = L.heads, L.head_dim
+        strm = stream or torch.cuda.current_stream()
+        smax = max(L.chunk_len(i) for i in range(N))
+        G = max(1, int(group))
+        key = ("ring", window, smax)
+        if getattr(self, "_ring_key", None) != key:
+            self._ring = torch.empty((2, window, 2, smax, h, d), dtype=self.o.dtype, device=self.device)
+            self._ring_key = key
+        ring = self._ring
+        gkey = ("grp", G, smax)
+        if getattr(self, "_grp_key", None) != gkey:
+            f32 = dict(dtype=torch.float32, device=self.device)
+            self._grp = [dict(o_acc=torch.empty((smax, h, d), **f32), m=torch.empty((smax * h,), **f32),
+                              l=torch.empty((smax * h,), **f32), delta=torch.empty((smax * h,), **f32),
+                              dq_acc=torch.empty((smax, h, d), **f32)) for _ in range(G)]
+            self._grp_key = gkey
+        scr = self._grp
+        stats = {"d2h": 0, "h2d": 0, "windows": 0, "group": G}
+        off_done = {}
+
+        def host_of(j):
+            nb = L.chunk_len(j) * h * d * self.elem
+            return self._host_buf(("k", j), nb), self._host_buf(("v", j), nb), nb
+
+        # steps: (kind, chunks of the group in processing order, windows); a window = (ids, where)
+        steps = []
+        for a in range(0, N, G):
+            C = list(range(a, min(N, a + G)))
+            dev_ids = [j for j in range(min(hot, C[-1] + 1))] + [j for j in range(max(hot, a - 1), C[-1] + 1)]
+            cold = list(range(hot, a - 1))
+            wins = [(dev_ids, "dev")] + [(cold[x:x + window], "ring") for x in range(0, len(cold), window)]
+            steps.append(("fwd", C, wins))
+        for b in range(N - 1, -1, -G):
+            C = list(range(b, max(-1, b - G), -1))
+            dev_ids = list(range(min(hot, b + 1)))
+            cold = list(range(hot, b + 1))
+            wins = ([(dev_ids, "dev")] if dev_ids else []) + \
+                [(cold[x:x + window], "ring") for x in range(0, len(cold), window)]
+            steps.append(("bwd", C, wins))
+        ring_windows = [(si, wi) for si, (_, _, ws) in enumerate(steps) for wi, w in enumerate(ws) if w[1] == "ring"]
+        ready = {}
+        offloaded = set(range(min(hot, N)))
+
+        def prefetch(n, must=False):
+            if n >= len(ring_windows) or n in ready:
+                return
+            si, wi = ring_windows[n]
+            ids = steps[si][2][wi][0]
+            if not all(j in offloaded for j in ids):
+                assert not must, "window streamed before its chunks were written back"
+                return
+            slot = n % 2
+            evs = []
+            for c, j in enumerate(ids):
+                if j in off_done:
+                    strm.wait_event(off_done.pop(j))
+                hk, hv, nb = host_of(j)
+                for which, hp in ((0, hk), (1, hv)):
+                    ev = torch.cuda.Event()
+                    self.ctx.kv_prefetch(j, hp, ring[slot, c, which, :L.chunk_len(j)], nb, consumer=strm, done=ev,
+                                         flags=sppo.SPPO_COPY_DEFER_WAIT)
+                    stats["h2d"] += nb
+                    evs.append(ev)
+            ready[n] = evs
+
+        self.dk_acc.zero_()
+        self.dv_acc.zero_()
+        n_ring = 0
+        prefetch(0)
+        for si, (kind, C, wins) in enumerate(steps):
+            # per chunk: its windows restricted to ids <= chunk, for FIRST / LAST
+            mine = {i: [wi for wi, (ids, _) in enumerate(wins) if any(j <= i for j in ids)] for i in C}
+            for wi, (ids, where) in enumerate(wins):
+                if where == "ring":
+                    prefetch(n_ring, must=True)
+                    prefetch(n_ring + 1)
+                    for ev in ready.pop(n_ring):
+                        strm.wait_event(ev)
+                    slot = n_ring % 2
+                    ks_all = [ring[slot, c, 0, :L.chunk_len(j)] for c, j in enumerate(ids)]
+                    vs_all = [ring[slot, c, 1, :L.chunk_len(j)] for c, j in enumerate(ids)]
+                    n_ring += 1
+                else:
+                    ks_all = [self.rows(k, j) for j in ids]
+                    vs_all = [self.rows(v, j) for j in ids]
+                stats["windows"] += 1
+                for gi, i in enumerate(C):
+                    sel = [c for c, j in enumerate(ids) if j <= i]
+                    if not sel:
+                        continue
+                    my = mine[i]
+                    flags = (sppo.SPPO_FIRST if wi == my[0] else 0) | (sppo.SPPO_LAST if wi == my[-1] else 0)
+                    wids = [ids[c] for c in sel]
+                    ks, vs = [ks_all[c] for c in sel], [vs_all[c] for c in sel]
+                    s = L.chunk_len(i)
+                    sc = scr[gi]
+                    if kind == "fwd":
+                        self.ctx.attn_fwd(L, i, self.rows(q, i), wids, ks, vs, flags=flags,
+                                          state=None if len(my) == 1 else (sc["o_acc"][:s], sc["m"][:s * h], sc["l"][:s * h]),
+                                          o=self.rows(self.o, i), lse=self.lse_view(i), stream=strm)
+                        self.launches += 1
+                    else:
+                        has_i = i in wids
+                        self.ctx.attn_bwd(L, i, self.rows(q, i), wids, ks, vs, self.rows(self.o, i), self.lse_view(i),
+                                          self.rows(do, i), sc["delta"][:s * h], sc["dq_acc"][:s],
+                                          [self.rows(self.dk_acc, j) for j in wids],
+                                          [self.rows(self.dv_acc, j) for j in wids],
+                                          dq=self.rows(self.dq, i), dk=self.rows(self.dk, i) if has_i else None,
+                                          dv=self.rows(self.dv, i) if has_i else None, flags=flags, stream=strm)
+                        self.launches += 1 + (flags & sppo.SPPO_FIRST != 0) + (flags & sppo.SPPO_LAST != 0)
+            if kind == "fwd":
+                last_ev = None
+                for i in C:
+                    if i < hot:
+                        continue
+                    hk, hv, nb = host_of(i)
+                    ev = torch.cuda.Event()
+                    stats["d2h"] += self.ctx.kv_offload(i, self.rows(k, i), hk, nb, 1.0, producer=strm)
+                    stats["d2h"] += self.ctx.kv_offload(i, self.rows(v, i), hv, nb, 1.0, producer=strm, done=ev)
+                    off_done[i] = ev
+                    offloaded.add(i)
+                    last_ev = ev
+                if poison:
+                    # chunks < C[-1] are never read from the device again (the next group's
+                    # device window starts at C[-1]); poison those whose host copy is complete
+                    for j in range(max(hot, C[0] - 1), C[-1]):
+                        if j in off_done:
+                            strm.wait_event(off_done[j])
+                        self.rows(k, j).view(torch.uint8).fill_(0xFF)
+                        self.rows(v, j).view(torch.uint8).fill_(0xFF)
+        return stats
+
     # end-to-end step through host buffers --------------------------------------
     def step_host_io(self, host_in, host_out, dev_in, stream=None):
         """One step whose inputs start in pinned host memory and whose results end

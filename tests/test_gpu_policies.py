@@ -157,3 +157,25 @@ def test_c_demo_runs():
     for args in ([], ["3000", "5", "3"], ["129", "2", "1"]):
         r = subprocess.run([exe] + args, capture_output=True, text=True, timeout=300)
         assert r.returncode == 0 and "PASS" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("hot,window,group", [(0, 2, 2), (2, 3, 2), (1, 2, 3), (0, 1, 4)])
+def test_kv_stream_grouped_matches_oracle(ctx, hot, window, group):
+    """Cold KV windows shared by `group` consecutive chunks (H2D volume / ~group),
+    device K/V of cold chunks poisoned: still the dense oracle's result."""
+    S, h, N = 2048, 2, 8
+    x, dev, eng = setup(ctx, S, h, N, seed=40 + hot + group)
+    k, v = dev["k"].clone(), dev["v"].clone()
+    base = eng.step_kv_stream(dev["q"], dev["k"].clone(), dev["v"].clone(), dev["do"], hot=hot, window=window)
+    stats = eng.step_kv_stream_grouped(dev["q"], k, v, dev["do"], hot=hot, window=window, group=group, poison=True)
+    torch.cuda.synchronize()
+    ctx.sync()
+    assert 0 < stats["h2d"] < base["h2d"]
+    xn = {kk: vv.double().numpy() for kk, vv in x.items()}
+    ref = oracle.causal_attention_dense_bwd(xn["q"], xn["k"], xn["v"], xn["do"])
+    np.testing.assert_allclose(eng.o.double().cpu().numpy(), ref["o"], **O_TOL)
+    for key in ("dq", "dk", "dv"):
+        np.testing.assert_allclose(getattr(eng, key).double().cpu().numpy(), ref[key], **G_TOL, err_msg=key)
+    if hot < N - group - 1:
+        assert torch.isnan(k[eng.L.offsets[hot]:eng.L.offsets[hot + 1]].float()).all()
+    eng.free_host()
