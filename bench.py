@@ -358,15 +358,21 @@ def run_ours(args, cfg, ws, rank, local):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            st = eng.step_kv_stream(x["q"], x["k"], x["v"], x["do"], hot=args.kv_hot, window=args.kv_window,
-                                    stream=stream)
+            if args.kv_group > 1:
+                st = eng.step_kv_stream_grouped(x["q"], x["k"], x["v"], x["do"], hot=args.kv_hot,
+                                                window=args.kv_window, group=args.kv_group, stream=stream)
+            else:
+                st = eng.step_kv_stream(x["q"], x["k"], x["v"], x["do"], hot=args.kv_hot, window=args.kv_window,
+                                        stream=stream)
             e1.record(stream)
             torch.cuda.synchronize()
             if rep > 0:
                 res.append(e0.elapsed_time(e1))
         kv_ms = max_over_ranks(statistics.median(res), ws)
         kvs = {"policy": f"kv hot-prefix P={args.kv_hot} resident, chunks >= P streamed H2D in windows of "
-                         f"{args.kv_window} (2-slot ring) for every later fwd/bwd; Type-1 resident",
+                         f"{args.kv_window} (2-slot ring) for every later fwd/bwd"
+                         + (f", each window shared by {args.kv_group} consecutive chunks" if args.kv_group > 1 else "")
+                         + "; Type-1 resident", "group": args.kv_group,
                "ms_per_step": round(kv_ms, 3), "resident_ms_per_step": round(ms, 3),
                "exposed_pct": round(100.0 * (kv_ms - ms) / ms, 2), "h2d_bytes": st["h2d"], "d2h_bytes": st["d2h"],
                "h2d_gbs_achieved": round(st["h2d"] / (kv_ms * 1e-3) / 1e9, 1), "windows": st["windows"],
@@ -846,6 +852,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--kv-hot", type=int, default=-1, help="also time KV streaming with this hot prefix (-1: skip)")
     ap.add_argument("--kv-window", type=int, default=4)
+    ap.add_argument("--kv-group", type=int, default=1, help="KV streaming: chunks sharing each streamed window")
     ap.add_argument("--fwd-streams", type=int, default=None, choices=[1, 2],
                     help="resident step: forward launches alternate over this many streams (default: by launch size)")
     ap.add_argument("--device-budget", type=float, default=0.0,
