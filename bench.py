@@ -638,7 +638,7 @@ def run_layer(args, cfg, ws, rank, local):
                    "d2h_ms_per_chunk_alpha1": [round(a / bw / 1e6, 3) for a in A], "bw_d2h_gbs_assumed": bw}
         lay.free_host()
 
-    # e2e: x, dz from pinned host memory in, z, dx back, around one step
+    # e2e: x, dz from pinned host memory in (chunk by chunk, overlapped), z, dx back after each chunk
     e2e = None
     if not args.no_e2e:
         nb = S * H * 2
@@ -649,25 +649,22 @@ def run_layer(args, cfg, ws, rank, local):
         ctx.sync()
         xin = {t: torch.empty_like(io[t]) for t in ("x", "dz")}
         res = []
+        h2d = d2h = 0
         for rep in range(3):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            for t in ("x", "dz"):
-                ctx.kv_prefetch(0, hin[t], xin[t], nb, consumer=stream)
-            out = lay.step(xin["x"], xin["dz"], stream)
-            ev = torch.cuda.Event()
-            ctx.kv_offload(0, out["z"], hout["z"], nb, 1.0, producer=stream)
-            ctx.kv_offload(0, out["dx"], hout["dx"], nb, 1.0, producer=stream, done=ev)
-            stream.wait_event(ev)
+            h2d, d2h, last = lay.step_host_io(hin["x"], hin["dz"], hout["z"], hout["dx"], xin["x"], xin["dz"], stream)
+            stream.wait_event(last)
             e1.record(stream)
             torch.cuda.synchronize()
             if rep > 0:
                 res.append(e0.elapsed_time(e1))
         e2e_ms = max_over_ranks(statistics.median(res), ws)
         e2e = {"value": round(fl * ws / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s", "ms_per_step": round(e2e_ms, 3),
-               "h2d_bytes_per_step": 2 * nb * ws, "d2h_bytes_per_step": 2 * nb * ws,
-               "path": "pinned host x, dz -> sppo_kv_prefetch; z, dx -> sppo_kv_offload (not overlapped)"}
+               "h2d_bytes_per_step": h2d * ws, "d2h_bytes_per_step": d2h * ws,
+               "path": "pinned host x (forward order), dz (backward order) -> chunk-wise sppo_kv_prefetch overlapped "
+                       "with compute; z after fwd(i), dx after bwd(i) -> sppo_kv_offload"}
         for ptr in list(hin.values()) + list(hout.values()):
             ctx.host_free(ptr)
 

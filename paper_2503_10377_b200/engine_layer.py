@@ -246,6 +246,50 @@ class ChunkedLayer:
             self.backward_chunk(i, x, dz, strm)
         return dict(z=self.z, dx=self.dx, grads=self.grads)
 
+    # ------------------------------------------------------------------ end to end through host buffers
+    def step_host_io(self, host_x, host_dz, host_z, host_dx, x, dz, stream=None):
+        """One step whose input x and upstream gradient dz start in pinned host
+        memory and whose results z, dx end there: x_i arrives H2D chunk by chunk in
+        forward order and dz_i in backward order (sppo_kv_prefetch, deferred waits:
+        the copies overlap compute), z_i leaves after fwd(i) and dx_i after bwd(i)
+        (sppo_kv_offload).  x, dz: device staging buffers [S, h].  Returns
+        (h2d_bytes, d2h_bytes, last_d2h_event)."""
+        strm = stream or torch.cuda.current_stream()
+        H, c = self.H, self.L.offsets
+        row = H * 2
+        ready_x, ready_dz = [], [None] * self.N
+        h2d = d2h = 0
+        for i in range(self.N):  # issue order = consumption order on the H2D stream
+            ev = torch.cuda.Event()
+            nb = (c[i + 1] - c[i]) * row
+            self.ctx.kv_prefetch(i, host_x + c[i] * row, self.rows(x, i), nb, consumer=strm, done=ev,
+                                 flags=sppo.SPPO_COPY_NO_ORDER | sppo.SPPO_COPY_DEFER_WAIT)
+            ready_x.append(ev)
+            h2d += nb
+        for i in range(self.N - 1, -1, -1):
+            ev = torch.cuda.Event()
+            nb = (c[i + 1] - c[i]) * row
+            self.ctx.kv_prefetch(i, host_dz + c[i] * row, self.rows(dz, i), nb, consumer=strm, done=ev,
+                                 flags=sppo.SPPO_COPY_NO_ORDER | sppo.SPPO_COPY_DEFER_WAIT)
+            ready_dz[i] = ev
+            h2d += nb
+        self._zero()
+        last = None
+        for i in range(self.N):
+            strm.wait_event(ready_x[i])
+            self.forward_chunk(i, x, strm)
+            nb = (c[i + 1] - c[i]) * row
+            last = torch.cuda.Event()
+            d2h += self.ctx.kv_offload(i, self.rows(self.z, i), host_z + c[i] * row, nb, 1.0, producer=strm, done=last)
+        for i in range(self.N - 1, -1, -1):
+            strm.wait_event(ready_dz[i])
+            self.backward_chunk(i, x, dz, strm)
+            nb = (c[i + 1] - c[i]) * row
+            last = torch.cuda.Event()
+            d2h += self.ctx.kv_offload(i, self.rows(self.dx, i), host_dx + c[i] * row, nb, 1.0, producer=strm,
+                                       done=last)
+        return h2d, d2h, last
+
     # ------------------------------------------------------------------ Type-1 offload with alpha
     def type1_bytes(self, i):
         """A_i: bytes of chunk i's Type-1 tensors."""

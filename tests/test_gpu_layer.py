@@ -171,3 +171,35 @@ def test_layer_pool_offload_equals_resident_and_frees_memory(ctx, alpha):
         a1 = lay.type1_bytes(0)
         assert peak_offload < peak_resident - a1, (peak_offload, peak_resident, a1)
     lay.free_host()
+
+
+def test_layer_host_io_step_equals_resident(ctx):
+    """x, dz streamed from pinned host memory chunk by chunk, z, dx back: the
+    host results equal the device step's."""
+    from paper_2503_10377_b200 import engine_layer, sppo
+    S, H, heads = 1024, 256, 2
+    params, io = _setup(S, H, 8)
+    dev = {k: v.cuda() for k, v in params.items()}
+    lay = engine_layer.ChunkedLayer(ctx, H, heads, sppo.partition_equal(S, 4), dev)
+    ref = lay.step(io["x"].cuda(), io["dz"].cuda())
+    z_ref, dx_ref = ref["z"].clone(), ref["dx"].clone()
+    nb = S * H * 2
+    hp = {t: ctx.host_alloc(nb) for t in ("x", "dz", "z", "dx")}
+    import ctypes
+    for t in ("x", "dz"):
+        ctypes.memmove(hp[t], io[t].contiguous().data_ptr(), nb)
+    xs, dzs = torch.empty((S, H), dtype=torch.bfloat16, device="cuda"), torch.empty((S, H), dtype=torch.bfloat16, device="cuda")
+    h2d, d2h, last = lay.step_host_io(hp["x"], hp["dz"], hp["z"], hp["dx"], xs, dzs)
+    last.synchronize()
+    torch.cuda.synchronize()
+    assert h2d == d2h == 2 * nb
+    out = {}
+    for t in ("z", "dx"):
+        buf = torch.empty((S, H), dtype=torch.bfloat16)
+        ctypes.memmove(buf.data_ptr(), hp[t], nb)
+        out[t] = buf
+    assert torch.equal(out["z"], z_ref.cpu())
+    rel = (out["dx"].double() - dx_ref.cpu().double()).norm() / dx_ref.cpu().double().norm()
+    assert rel < 1e-4
+    for p in hp.values():
+        ctx.host_free(p)
