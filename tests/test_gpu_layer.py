@@ -129,7 +129,7 @@ def test_layer_type1_offload_poisoned_equals_resident(ctx):
     lay.free_host()
 
 
-@pytest.mark.parametrize("alpha", [[1.0, 1.0, 1.0, 0.0], [0.3, 0.7, 1.0, 0.0], [0.0, 0.5, 0.0, 0.0]])
+@pytest.mark.parametrize("alpha", [[1.0] * 7 + [0.0], [0.3, 0.7] + [1.0] * 5 + [0.0], [0.0, 0.5] + [0.0] * 6])
 def test_layer_pool_offload_equals_resident_and_frees_memory(ctx, alpha):
     """pool mode: chunk activation sets are separate allocations released after
     their D2H (suffix 1 - alpha kept compactly) and rebuilt before bwd(i).
@@ -137,10 +137,10 @@ def test_layer_pool_offload_equals_resident_and_frees_memory(ctx, alpha):
     order); the peak device memory of the offloaded step is below the
     all-resident step's when every chunk but the last is fully offloaded."""
     from paper_2503_10377_b200 import engine_layer, sppo
-    S, H, heads = 2048, 512, 4
+    S, H, heads = 4096, 512, 4
     params, io = _setup(S, H, 6)
     dev = {k: v.cuda() for k, v in params.items()}
-    off = sppo.partition_equal(S, 4)
+    off = sppo.partition_equal(S, 8)
     x, dz = io["x"].cuda(), io["dz"].cuda()
     ref_lay = engine_layer.ChunkedLayer(ctx, H, heads, off, dev)
     r = ref_lay.step(x, dz)
@@ -168,8 +168,10 @@ def test_layer_pool_offload_equals_resident_and_frees_memory(ctx, alpha):
         # atomics), which can flip bf16 roundings of dq / da downstream: 1.2e-5 seen
         assert rel < 1e-4, (k, float(rel))
     if alpha[0] == 1.0:
+        # resident: all 8 chunk sets alive at the forward/backward turn; offloaded: at
+        # most ~2 pending D2H + the current + the last (alpha 0) + 2 prefetched
         a1 = lay.type1_bytes(0)
-        assert peak_offload < peak_resident - a1, (peak_offload, peak_resident, a1)
+        assert peak_offload < peak_resident - 2 * a1, (peak_offload, peak_resident, a1)
     lay.free_host()
 
 
