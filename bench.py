@@ -547,7 +547,7 @@ def run_layer(args, cfg, ws, rank, local):
     offsets = layer_offsets(args, S, N, H)
     params = synth.make_layer_params(H, 0, device=dev)
     io = synth.make_layer_io(S, H, 0, device=dev)
-    lay = engine_layer.ChunkedLayer(ctx, H, heads, offsets, params, device=dev)
+    lay = engine_layer.ChunkedLayer(ctx, H, heads, offsets, params, device=dev, streams=args.layer_streams)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         lay.step(io["x"], io["dz"], stream)
@@ -680,6 +680,7 @@ def run_layer(args, cfg, ws, rank, local):
             "config": {"workload": cfg["workload"].replace("attention layer", "layer") + " -- full GPT layer "
                                    f"(hidden {H}, MLP 4x, LayerNorm, GELU) per chunk",
                        "hidden": H, "heads": heads, "seq_len": S, "chunks": N, "partition": args.partition,
+                       "streams": args.layer_streams,
                        "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
                        "l2": "inputs larger than L2 (activations GBs per step)"},
             "tokens_per_s": round(S * ws / (ms * 1e-3), 1), "pct_of_bf16_peak": round(100 * tflops / peaks["burst"], 2),
@@ -856,6 +857,8 @@ def main():
                     help="GB of device memory for the step: picks the KV hot prefix that fits (0: off)")
     ap.add_argument("--partition", default="equal", choices=["equal", "balanced", "layer-balanced"])
     ap.add_argument("--shard-of", type=int, default=1, help="1 GPU: run rank 0's heads of a G-GPU split")
+    ap.add_argument("--layer-streams", type=int, default=1, choices=[1, 2],
+                    help="layer workload: 2 = token-wise halves of chunk i overlap chunk i+1's attention phase")
     ap.add_argument("--layer-pool", action="store_true",
                     help="layer workload with activation sets freed after offload (fits C3's 1M tokens)")
     ap.add_argument("--workload", default="attention", choices=["attention", "layer"],

@@ -53,7 +53,7 @@ LN_EPS = 1e-5
 
 class ChunkedLayer:
     def __init__(self, ctx: sppo.Context, hidden: int, heads: int, offsets, params: dict, device="cuda",
-                 timing: bool = False, pool: bool = False):
+                 timing: bool = False, pool: bool = False, streams: int = 1):
         self.ctx = ctx
         self.H, self.heads = hidden, heads
         self.d = hidden // heads
@@ -79,8 +79,12 @@ class ChunkedLayer:
         # per-chunk backward scratch (longest chunk)
         smax = max(self.L.chunk_len(i) for i in range(self.N))
         self.du = torch.empty((smax, 4 * H), **bf)
-        for n in ("dbn", "dy", "da", "d_o", "dq", "dkc", "dvc"):
+        for n in ("dbn", "da", "dq", "dkc", "dvc"):
             setattr(self, n, torch.empty((smax, H), **bf))
+        # d_o and dy pass from backward_b(i) to backward_a(i): two sets, so that
+        # backward_b(i-1) on a second stream can run while backward_a(i) reads them
+        self.dy2 = [torch.empty((smax, H), **bf) for _ in range(2)]
+        self.d_o2 = [torch.empty((smax, H), **bf) for _ in range(2)]
         self.dq_acc = torch.empty((smax, H), **f32)
         self.delta = torch.empty((smax * heads,), **f32)
         # Type-1: whole-sequence buffers (resident) or per-chunk allocations (pool)
@@ -95,6 +99,8 @@ class ChunkedLayer:
         self.gemm_events = None  # list: (start, end, FLOPs) of every GEMM call (bench instrumentation)
         self.attn_events = None  # list: (start, end) of every attention call
         self._host = {}
+        self.streams = streams
+        self._side = None
 
     # ------------------------------------------------------------------ helpers
     def rows(self, t, i):
@@ -158,8 +164,15 @@ class ChunkedLayer:
 
     # ------------------------------------------------------------------ forward of chunk i
     def forward_chunk(self, i, x, strm):
-        p, H, s = self.p, self.H, self.L.chunk_len(i)
         end = self._ev("fwd", strm)
+        self.forward_a(i, x, strm)
+        self.forward_b(i, x, strm)
+        if end is not None:
+            end.record(strm)
+
+    def forward_a(self, i, x, strm):
+        """LN1, QKV projection, attention of chunk i (needs K/V of chunks <= i)."""
+        p, H, s = self.p, self.H, self.L.chunk_len(i)
         T = self.T[i] = self._t1_set(i)
         xi = self.rows(x, i)
         self.ctx.layernorm_fwd(xi, p["ln1_g"], p["ln1_b"], T["a"], T["mu1"], T["rstd1"], eps=LN_EPS, stream=strm)
@@ -170,26 +183,38 @@ class ChunkedLayer:
         self.ctx.attn_fwd(self.L, i, T["q"], ids, ks, vs, o=T["o"], lse=T["lse"], stream=strm)
         if ae is not None:
             ae.record(strm)
-        self._gemm(s, H, H, T["o"], p["w_o"], T["y"], bias=p["b_o"], residual=xi, stream=strm)
+        self.launches += 2
+
+    def forward_b(self, i, x, strm):
+        """Out-projection + residual, LN2, MLP of chunk i (needs only forward_a(i))."""
+        p, H, s = self.p, self.H, self.L.chunk_len(i)
+        T = self.T[i]
+        self._gemm(s, H, H, T["o"], p["w_o"], T["y"], bias=p["b_o"], residual=self.rows(x, i), stream=strm)
         self.ctx.layernorm_fwd(T["y"], p["ln2_g"], p["ln2_b"], T["b"], T["mu2"], T["rstd2"], eps=LN_EPS,
                                stream=strm)
         self._gemm(s, 4 * H, H, T["b"], p["w_1"], T["g"], bias=p["b_1"], aux_out=T["u"],
                    epilogue=sppo.SPPO_EPI_GELU, stream=strm)
         self._gemm(s, H, 4 * H, T["g"], p["w_2"], self.rows(self.z, i), bias=p["b_2"], residual=T["y"],
                    stream=strm)
-        self.launches += 3
-        if end is not None:
-            end.record(strm)
+        self.launches += 1
 
     # ------------------------------------------------------------------ backward of chunk i
     def backward_chunk(self, i, x, dz, strm):
-        p, gr, H, s = self.p, self.grads, self.H, self.L.chunk_len(i)
         end = self._ev("bwd", strm)
+        self.backward_b(i, x, dz, strm)
+        self.backward_a(i, x, dz, strm)
+        if end is not None:
+            end.record(strm)
+
+    def backward_b(self, i, x, dz, strm, buf=0):
+        """MLP, LN2 and out-projection backward of chunk i (needs only dz_i): writes
+        d_o and dy into scratch set `buf`; accumulates w_2, w_1, w_o, LN2 gradients."""
+        p, gr, H, s = self.p, self.grads, self.H, self.L.chunk_len(i)
         T = self.T[i]
         ctx = self.ctx
-        du, dbn, dy, da, d_o = self.du[:s], self.dbn[:s], self.dy[:s], self.da[:s], self.d_o[:s]
-        dq, dk, dv = self.dq[:s], self.dkc[:s], self.dvc[:s]
-        dzi, xi = self.rows(dz, i), self.rows(x, i)
+        du, dbn = self.du[:s], self.dbn[:s]
+        dy, d_o = self.dy2[buf][:s], self.d_o2[buf][:s]
+        dzi = self.rows(dz, i)
         acc = sppo.SPPO_EPI_ACC_F32
         # MLP: fc2 then fc1
         self._gemm(s, 4 * H, H, dzi, p["w_2"], du, b_mn=1, aux_in=T["u"], epilogue=sppo.SPPO_EPI_DGELU, stream=strm)
@@ -206,6 +231,18 @@ class ChunkedLayer:
         self._gemm(s, H, H, dy, p["w_o"], d_o, b_mn=1, stream=strm)
         self._gemm(H, H, s, dy, T["o"], gr["w_o"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
         ctx.col_reduce(dy, s, H, gr["b_o"], stream=strm)
+        self.launches += 5
+
+    def backward_a(self, i, x, dz, strm, buf=0):
+        """Attention backward of chunk i (after chunk i+1's), QKV projection and LN1
+        backward; reads d_o / dy of scratch set `buf`."""
+        p, gr, H, s = self.p, self.grads, self.H, self.L.chunk_len(i)
+        T = self.T[i]
+        ctx = self.ctx
+        da, dy, d_o = self.da[:s], self.dy2[buf][:s], self.d_o2[buf][:s]
+        dq, dk, dv = self.dq[:s], self.dkc[:s], self.dvc[:s]
+        xi = self.rows(x, i)
+        acc = sppo.SPPO_EPI_ACC_F32
         # attention of chunk i against K/V of chunks 0..i; dK_i, dV_i final afterwards (L11)
         ids, ks, vs = self._kv(i)
         ae = self._attn_ev(strm)
@@ -221,11 +258,9 @@ class ChunkedLayer:
         ctx.layernorm_bwd(da, xi, p["ln1_g"], T["mu1"], T["rstd1"], self.rows(self.dx, i), dres=dy, stream=strm)
         ctx.col_reduce(da, s, H, gr["ln1_b"], x=xi, mean=T["mu1"], rstd=T["rstd1"], prod_acc=gr["ln1_g"],
                        stream=strm)
-        self.launches += 3 + 8  # attention bwd (Delta preprocess, main, dQ cast) + LN / column reductions
+        self.launches += 3 + 3  # attention bwd (Delta preprocess, main, dQ cast) + LN1 bwd + 2 column reductions
         if self.pool:
             self.T[i] = None  # released: later allocations on this stream are ordered after these kernels
-        if end is not None:
-            end.record(strm)
 
     def _zero(self):
         for t in self.grads.values():
@@ -235,15 +270,45 @@ class ChunkedLayer:
 
     # ------------------------------------------------------------------ one step, no offload
     def step(self, x, dz, stream=None, mark=None):
-        """Forward over chunks 0..N-1 then backward over N-1..0, nothing offloaded."""
+        """Forward over chunks 0..N-1 then backward over N-1..0, nothing offloaded.
+        With ``self.streams == 2`` the token-wise halves run on a second stream:
+        forward_b(i) (out-proj, MLP) overlaps forward_a(i+1) (QKV, attention), and
+        backward_b(i-1) overlaps backward_a(i) — the chunk-level parallelism the
+        layer has inside one GPU (the attention of chunk i+1 does not depend on
+        chunk i's MLP), which fills the tails of each other's launches."""
         strm = stream or torch.cuda.current_stream()
         self._zero()
+        if self.streams < 2 or self.timing:
+            for i in range(self.N):
+                self.forward_chunk(i, x, strm)
+            if mark is not None:
+                mark.record(strm)
+            for i in range(self.N - 1, -1, -1):
+                self.backward_chunk(i, x, dz, strm)
+            return dict(z=self.z, dx=self.dx, grads=self.grads)
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        s2 = self._side
+        ev = lambda st: (lambda e: (e.record(st), e)[1])(torch.cuda.Event())  # noqa: E731
+        s2.wait_event(ev(strm))  # zeroed accumulators
         for i in range(self.N):
-            self.forward_chunk(i, x, strm)
+            self.forward_a(i, x, strm)
+            s2.wait_event(ev(strm))
+            self.forward_b(i, x, s2)
+        strm.wait_event(ev(s2))
         if mark is not None:
             mark.record(strm)
+        s2.wait_event(ev(strm))
+        done_a = {}
         for i in range(self.N - 1, -1, -1):
-            self.backward_chunk(i, x, dz, strm)
+            buf = i % 2
+            if i + 2 in done_a:
+                s2.wait_event(done_a.pop(i + 2))  # backward_a(i+2) has read scratch set `buf`
+            self.backward_b(i, x, dz, s2, buf)
+            strm.wait_event(ev(s2))
+            self.backward_a(i, x, dz, strm, buf)
+            done_a[i] = ev(strm)
+        strm.wait_event(ev(s2))
         return dict(z=self.z, dx=self.dx, grads=self.grads)
 
     # ------------------------------------------------------------------ end to end through host buffers

@@ -205,3 +205,27 @@ def test_layer_host_io_step_equals_resident(ctx):
     assert rel < 1e-4
     for p in hp.values():
         ctx.host_free(p)
+
+
+def test_layer_two_stream_step_equals_one_stream(ctx):
+    """streams=2: forward_b(i) / backward_b(i-1) on a second stream overlap the next
+    chunk's attention phase; results equal the single-stream step (forward bitwise,
+    gradients to fp32 reduction order)."""
+    from paper_2503_10377_b200 import engine_layer, sppo
+    S, H, heads = 2048, 256, 2
+    params, io = _setup(S, H, 9)
+    dev = {k: v.cuda() for k, v in params.items()}
+    off = sppo.partition_equal(S, 8)
+    x, dz = io["x"].cuda(), io["dz"].cuda()
+    one = engine_layer.ChunkedLayer(ctx, H, heads, off, dev)
+    r = one.step(x, dz)
+    ref = {"z": r["z"].clone(), "dx": r["dx"].clone(), **{k: v.clone() for k, v in r["grads"].items()}}
+    two = engine_layer.ChunkedLayer(ctx, H, heads, off, dev, streams=2)
+    for _ in range(2):
+        o = two.step(x, dz)
+        torch.cuda.synchronize()
+        assert torch.equal(o["z"], ref["z"])
+        for k in ["dx"] + list(L.PARAM_NAMES):
+            got = o["dx"] if k == "dx" else o["grads"][k]
+            rel = (got.double() - ref[k].double()).norm() / ref[k].double().norm()
+            assert rel < 1e-4, (k, float(rel))
