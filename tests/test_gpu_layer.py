@@ -229,3 +229,12 @@ def test_layer_two_stream_step_equals_one_stream(ctx):
             got = o["dx"] if k == "dx" else o["grads"][k]
             rel = (got.double() - ref[k].double()).norm() / ref[k].double().norm()
             assert rel < 1e-4, (k, float(rel))
+
+
+@pytest.mark.slow
+def test_layer_step_gpt7b_width_matches_oracle(ctx):
+    """The GPT-7B layer width of the bench (hidden 4096, 32 heads, MLP 16384) on
+    4096 tokens in 2 chunks: every GEMM at its production K / N (K up to 16384,
+    N up to 16384, the CTA-pair kernel over many tiles), full fwd + bwd against
+    the fp64 oracle (~5 TFLOP of fp64 on the host: tens of seconds)."""
+    _run_and_compare(ctx, 4096, 4096, 32, [0, 2048, 4096], seed=11)
