@@ -66,6 +66,10 @@ constexpr int kDqBufs = 2;
 #ifndef SPPO_EPI_RED
 #define SPPO_EPI_RED 1  // measured: bwd +3 % at C2, +9 % at 2K chunks vs load-add-store
 #endif
+#ifndef SPPO_BWD_EMU_EVERY
+#define SPPO_BWD_EMU_EVERY 0  // 1 of every N exp2 pairs of P on the FMA pipe (cubic, as the forward); 0 = off
+#endif
+constexpr int kBwdEmu = SPPO_BWD_EMU_EVERY;
 constexpr bool kEpiRed = SPPO_EPI_RED;  // dK/dV accumulator epilogue: red.global.add (1) or load-add-store (0)  // 4 buffers measured slower: the reduces queue ahead of Q/dO loads on the TMA unit
 constexpr uint32_t kOffDQ = kOffDS + kTile;       // kDqBufs x [128 rows][32 fp32] reduce staging
 constexpr uint32_t kOffLSE = kOffDQ + kDqBufs * 16384;  // 2 x 128 fp32 (LSE * log2 e)
@@ -456,8 +460,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             x1.x = (j + 2 >= first_vis) ? x1.x : -INFINITY;
             x1.y = (j + 3 >= first_vis) ? x1.y : -INFINITY;
           }
-          pr[c2] = make_float2(ex2(x0.x), ex2(x0.y));
-          pr[c2 + 1] = make_float2(ex2(x1.x), ex2(x1.y));
+          if (kBwdEmu > 0 && c2 % kBwdEmu == kBwdEmu - 1)
+            pr[c2] = ex2_poly2(x0);
+          else
+            pr[c2] = make_float2(ex2(x0.x), ex2(x0.y));
+          if (kBwdEmu > 0 && (c2 + 1) % kBwdEmu == kBwdEmu - 1)
+            pr[c2 + 1] = ex2_poly2(x1);
+          else
+            pr[c2 + 1] = make_float2(ex2(x1.x), ex2(x1.y));
           pk[c2] = pack_bf16(pr[c2].x, pr[c2].y);
           pk[c2 + 1] = pack_bf16(pr[c2 + 1].x, pr[c2 + 1].y);
         }

@@ -78,25 +78,6 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return d;
 }
 
-// 2^x for a pair on the FMA pipe: x = floor + f, 2^f by a cubic fitted for
-// relative error <= 8.6e-5 on [0,1) (far below the bf16 rounding of P).
-__device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  const float kRound = 12582912.f;  // 2^23 + 2^22: adding it (round-down) leaves floor(x) in the low bits
-  x.x = fmaxf(x.x, -127.f);
-  x.y = fmaxf(x.y, -127.f);
-  float2 r;
-  asm("add.rm.f32x2 %0, %1, %2;"
-      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
-      : "l"(*reinterpret_cast<unsigned long long*>(&x)), "l"(0x4B4000004B400000ull));
-  const float2 fl = fadd2(r, make_float2(-kRound, -kRound));
-  const float2 f = fadd2(x, make_float2(-fl.x, -fl.y));
-  float2 p = ffma2(make_float2(0.07706520f, 0.07706520f), f, make_float2(0.22764701f, 0.22764701f));
-  p = ffma2(p, f, make_float2(0.69511634f, 0.69511634f));
-  p = ffma2(p, f, make_float2(1.f, 1.f));
-  // add floor(x) to the exponent field
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(r.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(r.y) << 23)));
-}
 
 __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant__ Sm100Fwd a) {
   extern __shared__ uint8_t smem_raw[];
