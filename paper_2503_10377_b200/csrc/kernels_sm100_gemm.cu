@@ -287,8 +287,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 // rows x 256 columns.  Both CTAs' TMA loads complete on the leader's full
 // barrier; MMA commits multicast to both CTAs; both CTAs' epilogue threads
 // release an accumulator buffer on the leader's acc_empty barrier.
-constexpr int kPairStages = 6;
-constexpr uint32_t kPairA = 128 * BK * 2, kPairB = 128 * BK * 2, kPairStage = kPairA + kPairB;
+#ifndef SPPO_GEMM_PAIR_BK
+#define SPPO_GEMM_PAIR_BK 128  // measured: 128 vs 64 -> x W^T 1444-1519 vs 1330-1373 TF/s, dy W 1471 vs 1162-1249
+#endif
+// K depth of one pipeline stage (64 | 128).  The MMA issuer waits on one barrier
+// and commits once per stage, so a deeper stage (8 MMAs instead of 4) halves that
+// per-stage overhead on the issue path, which runs nearly synchronously with the
+// tensor pipe; 3 stages x 64 KB still fill the 192 KB ring.
+constexpr int PBK = SPPO_GEMM_PAIR_BK;
+constexpr int kPairStages = PBK == 64 ? 6 : 3;
+constexpr uint32_t kPairA = 128 * PBK * 2, kPairB = 128 * PBK * 2, kPairStage = kPairA + kPairB;
+constexpr uint32_t kPairMnBlock = 64 * PBK * 2;  // one 64-wide MN block over the stage's K depth
 constexpr int kPairSmem = kPairStages * kPairStage + 1024;
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -301,7 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = warp_id(), lane = lane_id();
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int Mt = (p.M + 255) / 256, Nt = p.N / 256, Kt = (p.K + BK - 1) / BK;
+  const int Mt = (p.M + 255) / 256, Nt = p.N / 256, Kt = (p.K + PBK - 1) / PBK;
   const int tiles = Mt * Nt;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
@@ -343,23 +352,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           uint8_t* sB = sA + kPairA;
           if (leader) mbar_arrive_expect_tx(&bars.full[stage], 2 * kPairStage);
           const uint32_t Lf = mapa(smem_u32(&bars.full[stage]), 0);
-          const int k0 = kb * BK;
-          if (!p.a_mn) {
-            const int part = k0 / p.a_part_w;
-            const CUtensorMap* m = part == 0 ? &ta0 : (part == 1 ? &ta1 : &ta2);
-            tma_load_2d_pair(sA, m, Lf, k0 - part * p.a_part_w, m0);
-          } else {
-            const int part = m0 / p.a_part_w;
-            const CUtensorMap* m = part == 0 ? &ta0 : (part == 1 ? &ta1 : &ta2);
-            const int mc = m0 - part * p.a_part_w;
-            tma_load_2d_pair(sA, m, Lf, mc, k0);
-            tma_load_2d_pair(sA + kMnBox, m, Lf, mc + 64, k0);
-          }
-          if (!p.b_mn) {
-            tma_load_2d_pair(sB, &tb, Lf, k0, n0);
-          } else {
-            tma_load_2d_pair(sB, &tb, Lf, n0, k0);
-            tma_load_2d_pair(sB + kMnBox, &tb, Lf, n0 + 64, k0);
+          const int k0 = kb * PBK;
+#pragma unroll
+          for (int h = 0; h < PBK / 64; ++h) {  // 64-deep K halves of the stage
+            const int kh = k0 + 64 * h;
+            if (!p.a_mn) {  // K-major: box h at +16 KB * h
+              const int part = kh / p.a_part_w;
+              const CUtensorMap* m = part == 0 ? &ta0 : (part == 1 ? &ta1 : &ta2);
+              tma_load_2d_pair(sA + h * 16384, m, Lf, kh - part * p.a_part_w, m0);
+            } else {  // MN-major: block b (64 MN) holds all PBK K rows, half h at +8 KB * h
+              const int part = m0 / p.a_part_w;
+              const CUtensorMap* m = part == 0 ? &ta0 : (part == 1 ? &ta1 : &ta2);
+              const int mc = m0 - part * p.a_part_w;
+              tma_load_2d_pair(sA + h * kMnBox, m, Lf, mc, kh);
+              tma_load_2d_pair(sA + kPairMnBlock + h * kMnBox, m, Lf, mc + 64, kh);
+            }
+            if (!p.b_mn) {
+              tma_load_2d_pair(sB + h * 16384, &tb, Lf, kh, n0);
+            } else {
+              tma_load_2d_pair(sB + h * kMnBox, &tb, Lf, n0, kh);
+              tma_load_2d_pair(sB + kPairMnBlock + h * kMnBox, &tb, Lf, n0 + 64, kh);
+            }
           }
           if (++stage == kPairStages) {
             stage = 0;
@@ -372,9 +385,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (leader) {
       const uint32_t idesc = idesc_bf16(256, 256, p.a_mn, p.b_mn);
       const uint32_t sbase = smem_u32(smem);
-      const uint64_t a0 = p.a_mn ? sdesc_mnmajor(sbase, kMnBox) : sdesc_kmajor(sbase);
-      const uint64_t b0 = p.b_mn ? sdesc_mnmajor(sbase + kPairA, kMnBox) : sdesc_kmajor(sbase + kPairA);
-      const uint32_t a_k = (p.a_mn ? 2048u : 32u) >> 4, b_k = (p.b_mn ? 2048u : 32u) >> 4;
+      const uint64_t a0 = p.a_mn ? sdesc_mnmajor(sbase, kPairMnBlock) : sdesc_kmajor(sbase);
+      const uint64_t b0 = p.b_mn ? sdesc_mnmajor(sbase + kPairA, kPairMnBlock) : sdesc_kmajor(sbase + kPairA);
+      // K=16 step k: MN-major +2 KB * k (the K halves of a block are contiguous);
+      // K-major +32 B * (k % 4) within a 64-deep box, +16 KB per box
+      auto koff = [](int k, int mn) -> uint64_t {
+        return (uint64_t)((mn ? 2048u * k : 16384u * (k >> 2) + 32u * (k & 3)) >> 4);
+      };
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -388,8 +405,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint64_t so = (uint64_t)((stage * kPairStage) >> 4);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            mma2_ss_w(d, a0 + so + k * a_k, b0 + so + k * b_k, idesc, (kb | k) != 0);
+          for (int k = 0; k < PBK / 16; ++k)
+            mma2_ss_w(d, a0 + so + koff(k, p.a_mn), b0 + so + koff(k, p.b_mn), idesc, (kb | k) != 0);
           mma2_commit_w(&bars.empty[stage]);
           if (++stage == kPairStages) {
             stage = 0;

@@ -98,14 +98,15 @@ sppo_status sppo_gemm(sppo_ctx ctx, const sppo_gemm_args* g, void* stream) {
 
   const int64_t cpw = g->N / g->c_parts;
   int bn = (cpw % 256 == 0) ? 256 : 128;
-  // CTA pair (cluster of 2, 256 x 256 tiles) when N tiles are 256 wide, M spans
-  // more than one 128-row tile and both operands are K-major (measured at the
-  // GPT-7B chunk shapes, tools/gemm_bench.py: pair 1395-1403 vs single 1307-1314
-  // TF/s for x W^T; with an MN-major operand the pair was slower, 1063-1152 vs
-  // 1190-1318).  SPPO_GEMM_PAIR=0 / 2 forces the single-CTA / pair kernel.
+  // CTA pair (cluster of 2, 256 x 256 tiles, 128-deep K stages) whenever N tiles
+  // are 256 wide and M spans more than one 128-row tile, every operand
+  // orientation (measured at the GPT-7B chunk shapes, tools/gemm_bench.py, vs the
+  // single-CTA kernel: x W^T 1444-1519 vs 1330-1373 TF/s, dy W 1471-1473 vs
+  // 1162-1266, dy^T x 1180-1218 vs 1049-1152).  SPPO_GEMM_PAIR=0 selects the
+  // single-CTA kernel, =1 the pair only for K-major x K-major.
   static const int pair_env = [] {
     const char* e = getenv("SPPO_GEMM_PAIR");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 2;
   }();
   const bool pair = bn == 256 && g->M > 128 && (pair_env == 2 || (pair_env == 1 && !g->a_mn && !g->b_mn));
   CUtensorMap ta[3], tb;
