@@ -74,7 +74,20 @@ constexpr bool kEpiRed = SPPO_EPI_RED;  // dK/dV accumulator epilogue: red.globa
 constexpr uint32_t kOffDQ = kOffDS + kTile;       // kDqBufs x [128 rows][32 fp32] reduce staging
 constexpr uint32_t kOffLSE = kOffDQ + kDqBufs * 16384;  // 2 x 128 fp32 (LSE * log2 e)
 constexpr uint32_t kOffDelta = kOffLSE + 1024;    // 2 x 128 fp32
-constexpr uint32_t kOffBars = kOffDelta + 1024;
+#ifndef SPPO_BWD_FOLD
+#define SPPO_BWD_FOLD 0
+#endif
+// SPPO_BWD_FOLD: -LSE/tau and -Delta enter S^T and dP^T through one extra K=16
+// MMA step (A: a constant [keys][16] block with ones in k = 0, 1; B: per-tile
+// [q][16] blocks holding a bf16 hi/lo split of the statistic), so the compute
+// warps read no LSE / Delta from shared memory (their broadcast LDS.128 were
+// ~40 % of the kernel's LSU shared-memory wavefronts).  No-swizzle K-major core
+// matrices: element (row, k) at (row/8)*256 + (k/8)*128 + (row%8)*16 + (k%8)*2.
+constexpr bool kFold = SPPO_BWD_FOLD;
+constexpr uint32_t kOffXK = kOffDelta + 1024;   // [128 keys][16]: ones at k = 0, 1 (A of the extra step)
+constexpr uint32_t kOffXQ = kOffXK + 4096;      // [64 q][16]: -LSE/tau hi, lo (B of S^T's extra step)
+constexpr uint32_t kOffXO = kOffXQ + 2048;      // [64 q][16]: -Delta hi, lo (B of dP^T's extra step)
+constexpr uint32_t kOffBars = kFold ? kOffXO + 2048 : kOffDelta + 1024;
 constexpr uint32_t kSmemBytes = kOffBars + 256;
 static_assert(kSmemBytes <= 232448, "smem budget");
 
@@ -102,6 +115,11 @@ static_assert(sizeof(Bars) <= 256, "barrier block");
 
 __device__ __forceinline__ const CUtensorMap* tmap(const Sm100Bwd& a, int slot) {
   return reinterpret_cast<const CUtensorMap*>(a.desc_table) + slot;
+}
+
+// UMMA smem descriptor of a no-swizzle K-major operand (core matrices of 8 rows x 16 B)
+__device__ __forceinline__ uint64_t sdesc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return make_sdesc(saddr, lbo, sbo) & ~((uint64_t)7 << 61);
 }
 
 __device__ __forceinline__ uint32_t sw128(int r, int byte_in_row) {
@@ -144,8 +162,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     mbar_init(&bars.qb_empty, 1);
     mbar_init(&bars.ob_empty, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&bars.qa_full[s], 1);
-      mbar_init(&bars.oa_full[s], 1);
+      // fold: + one remote arrival per CTA once its extra B block is written
+      mbar_init(&bars.qa_full[s], kFold ? 3 : 1);
+      mbar_init(&bars.oa_full[s], kFold ? 3 : 1);
       mbar_init(&bars.qa_empty[s], 1);
       mbar_init(&bars.oa_empty[s], 1);
       mbar_init(&bars.lse_full[s], 32);
@@ -164,6 +183,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   if (warp == 14) tmem_alloc_pair<512>(&bars.tmem_base);
+  if (kFold) {
+    // constant parts of the extra K=16 operand blocks: ones block (A) and the
+    // all-zero k = 8..15 core matrices of the per-tile B blocks
+    const uint32_t one2 = 0x3F803F80u;  // bf16 (1, 1)
+    for (int r = threadIdx.x; r < 128; r += kThreads) {
+      *reinterpret_cast<uint4*>(smem + kOffXK + (r >> 3) * 256 + (r & 7) * 16) = make_uint4(one2, 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(smem + kOffXK + (r >> 3) * 256 + 128 + (r & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
+      if (r < 64) {
+        *reinterpret_cast<uint4*>(smem + kOffXQ + (r >> 3) * 256 + 128 + (r & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(smem + kOffXO + (r >> 3) * 256 + 128 + (r & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // barriers of both CTAs initialised before any remote arrive / complete_tx
@@ -200,12 +233,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int q0 = qtile(m) * BQ;
         const int sa = m % kStagesA, ua = m / kStagesA;  // stage and its use count
         if (ua > 0) mbar_wait(&bars.qa_empty[sa], (ua - 1) & 1);
+        if (kFold) {  // this CTA's 64 q rows of the tile: -LSE/tau as bf16 hi + lo at k = 0, 1
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = lane + 32 * e;
+            const int r = q0 + 64 * (int)rank + i;
+            const float cv = r < p.q_len ? -lse_h[r] / p.scale : -INFINITY;
+            const __nv_bfloat16 hi = __float2bfloat16_rn(cv);
+            const float lo = r < p.q_len ? cv - __bfloat162float(hi) : 0.f;
+            const __nv_bfloat162 hl = __halves2bfloat162(hi, __float2bfloat16_rn(lo));
+            *reinterpret_cast<uint4*>(smem + kOffXQ + (i >> 3) * 256 + (i & 7) * 16) =
+                make_uint4(*reinterpret_cast<const uint32_t*>(&hl), 0u, 0u, 0u);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+        }
         if (lane == 0) {
           const uint32_t L_qa = mapa(smem_u32(&bars.qa_full[sa]), 0);
           if (leader) mbar_arrive_expect_tx(&bars.qa_full[sa], 2 * kStageA);
           tma_load_3d_pair(smem + kOffQA + sa * kStageA, mq64, L_qa, 0, head, q0 + 64 * (int)rank);
           tma_load_3d_pair(smem + kOffQA + sa * kStageA + kHBox, mq64, L_qa, 64, head, q0 + 64 * (int)rank);
+          if (kFold) mbar_arrive_cluster(L_qa);
         }
+        if (kFold) continue;
         if (m >= 2) mbar_wait(&bars.lse_empty[s], ((m >> 1) - 1) & 1);
         float4 w;
         float* wp = reinterpret_cast<float*>(&w);
@@ -218,7 +268,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) TR(15, m);
         mbar_arrive(&bars.lse_full[s]);
       }
-      for (int m = max(M - 2, 0); m < M; ++m) mbar_wait(&bars.lse_empty[m & 1], (m >> 1) & 1);
+      if (!kFold)
+        for (int m = max(M - 2, 0); m < M; ++m) mbar_wait(&bars.lse_empty[m & 1], (m >> 1) & 1);
     } else if (warp == 15) {
       // ===================== TMA: dO rows half + Delta per tile =====================
       const CUtensorMap* mdo64 = tmap(a, a.do64_slot);
@@ -228,12 +279,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int q0 = qtile(m) * BQ;
         const int sa = m % kStagesA, ua = m / kStagesA;
         if (ua > 0) mbar_wait(&bars.oa_empty[sa], (ua - 1) & 1);
+        if (kFold) {  // this CTA's 64 q rows: -Delta as bf16 hi + lo at k = 0, 1
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = lane + 32 * e;
+            const int r = q0 + 64 * (int)rank + i;
+            const float cv = r < p.q_len ? -delta_h[r] : 0.f;
+            const __nv_bfloat16 hi = __float2bfloat16_rn(cv);
+            const __nv_bfloat162 hl = __halves2bfloat162(hi, __float2bfloat16_rn(cv - __bfloat162float(hi)));
+            *reinterpret_cast<uint4*>(smem + kOffXO + (i >> 3) * 256 + (i & 7) * 16) =
+                make_uint4(*reinterpret_cast<const uint32_t*>(&hl), 0u, 0u, 0u);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+        }
         if (lane == 0) {
           const uint32_t L_oa = mapa(smem_u32(&bars.oa_full[sa]), 0);
           if (leader) mbar_arrive_expect_tx(&bars.oa_full[sa], 2 * kStageA);
           tma_load_3d_pair(smem + kOffOA + sa * kStageA, mdo64, L_oa, 0, head, q0 + 64 * (int)rank);
           tma_load_3d_pair(smem + kOffOA + sa * kStageA + kHBox, mdo64, L_oa, 64, head, q0 + 64 * (int)rank);
+          if (kFold) mbar_arrive_cluster(L_oa);
         }
+        if (kFold) continue;
         if (m >= 2) mbar_wait(&bars.delta_empty[s], ((m >> 1) - 1) & 1);
         float4 w;
         float* wp = reinterpret_cast<float*>(&w);
@@ -245,7 +312,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         *reinterpret_cast<float4*>(sDelta + s * 128 + lane * 4) = w;
         mbar_arrive(&bars.delta_full[s]);
       }
-      for (int m = max(M - 2, 0); m < M; ++m) mbar_wait(&bars.delta_empty[m & 1], (m >> 1) & 1);
+      if (!kFold)
+        for (int m = max(M - 2, 0); m < M; ++m) mbar_wait(&bars.delta_empty[m & 1], (m >> 1) & 1);
     } else if (warp == 14) {
       // ===================== TMA: dO columns half, Q columns half per tile =====================
       const CUtensorMap* mq = tmap(a, a.q_slot);
@@ -306,7 +374,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         constexpr uint64_t kStageStep = kStageA >> 4;
         mbar_wait(&bars.qa_full[0], 0);
         tc_fence_after();
+        const uint64_t dXK = sdesc_noswz(smem_u32(smem + kOffXK), 128, 256);
+        const uint64_t dXQ = sdesc_noswz(smem_u32(smem + kOffXQ), 128, 256);
+        const uint64_t dXO = sdesc_noswz(smem_u32(smem + kOffXO), 128, 256);
         mma_kk(tS, dK_k, dQA_k);  // S^T(0) = K Q^T
+        if (kFold) mma2_ss_w(tS, dXK, dXQ, kIdescS, 1u);  // - LSE / tau
         mma2_commit_w(&bars.s_full);
         mma2_commit_w(&bars.qa_empty[0]);
         for (int m = 0; m < M; ++m) {
@@ -316,6 +388,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_after();
           TR(1, m);
           mma_kk(tdP, dV_k, dOA_k + (m % kStagesA) * kStageStep);  // dP^T = V dO^T
+          if (kFold) mma2_ss_w(tdP, dXK, dXO, kIdescS, 1u);  // - Delta
           mma2_commit_w(&bars.dp_full);
           mma2_commit_w(&bars.oa_empty[m % kStagesA]);
           mbar_wait(&bars.p_full, m & 1);
@@ -330,6 +403,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_after();
             TR(3, m);
             mma_kk(tS, dK_k, dQA_k + (n1 % kStagesA) * kStageStep);  // S^T(m+1): P(m) consumed (in-order pipe)
+            if (kFold) mma2_ss_w(tS, dXK, dXQ, kIdescS, 1u);
             mma2_commit_w(&bars.s_full);
             mma2_commit_w(&bars.qa_empty[n1 % kStagesA]);
           }
@@ -427,7 +501,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int s = m & 1;
       const int q0 = qtile(m) * BQ;
       const int qpos0 = p.q_start + q0 + g * 64;  // absolute position of this half's column 0
-      mbar_wait(&bars.lse_full[s], (m >> 1) & 1);
+      if (!kFold) mbar_wait(&bars.lse_full[s], (m >> 1) & 1);
       mbar_wait(&bars.s_full, m & 1);
 #ifndef SPPO_TRACE_DS
       if (lane == 0 && wq == 0) TR(6 + 4 * g, m);
@@ -450,9 +524,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (h == 1) tmem_wait_ld();
 #pragma unroll
         for (int c2 = 16 * h; c2 < 16 * h + 16; c2 += 2) {
-          const float4 l4 = *reinterpret_cast<const float4*>(lse2 + 2 * c2);
-          float2 x0 = ffma2(pr[c2], make_float2(sl2, sl2), make_float2(-l4.x, -l4.y));
-          float2 x1 = ffma2(pr[c2 + 1], make_float2(sl2, sl2), make_float2(-l4.z, -l4.w));
+          float2 x0, x1;
+          if (kFold) {  // S already holds s - LSE / tau
+            x0 = fmul2(pr[c2], make_float2(sl2, sl2));
+            x1 = fmul2(pr[c2 + 1], make_float2(sl2, sl2));
+          } else {
+            const float4 l4 = *reinterpret_cast<const float4*>(lse2 + 2 * c2);
+            x0 = ffma2(pr[c2], make_float2(sl2, sl2), make_float2(-l4.x, -l4.y));
+            x1 = ffma2(pr[c2 + 1], make_float2(sl2, sl2), make_float2(-l4.z, -l4.w));
+          }
           if (masked) {
             const int j = 2 * c2;
             x0.x = (j + 0 >= first_vis) ? x0.x : -INFINITY;
@@ -476,13 +556,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&bars.lse_empty[s]);  // every thread: its LSE reads are done
+      if (!kFold) mbar_arrive(&bars.lse_empty[s]);  // every thread: its LSE reads are done
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(L_p_full);
       if (lane == 0 && wq == 0 && g == 0) TR(7, m);
 
       // ---- dS = P (dP - Delta)   (tau is applied to dK / dQ at their write-out)
-      mbar_wait(&bars.delta_full[s], (m >> 1) & 1);
+      if (!kFold) mbar_wait(&bars.delta_full[s], (m >> 1) & 1);
       mbar_wait(&bars.dp_full, m & 1);
       if (lane == 0 && wq == 0 && g == 0) TR(8, m);
       tc_fence_after();
@@ -500,9 +580,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (h == 1) tmem_wait_ld();
 #pragma unroll
         for (int c2 = 16 * h; c2 < 16 * h + 16; c2 += 2) {
-          const float4 d4 = *reinterpret_cast<const float4*>(dl + 2 * c2);
-          const float2 t0 = fadd2(dp[c2], make_float2(-d4.x, -d4.y));
-          const float2 t1 = fadd2(dp[c2 + 1], make_float2(-d4.z, -d4.w));
+          float2 t0 = dp[c2], t1 = dp[c2 + 1];  // fold: dP already holds dP - Delta
+          if (!kFold) {
+            const float4 d4 = *reinterpret_cast<const float4*>(dl + 2 * c2);
+            t0 = fadd2(t0, make_float2(-d4.x, -d4.y));
+            t1 = fadd2(t1, make_float2(-d4.z, -d4.w));
+          }
           const float2 a0 = fmul2(pr[c2], t0);
           const float2 a1 = fmul2(pr[c2 + 1], t1);
           pk[c2] = pack_bf16(a0.x, a0.y);
@@ -518,7 +601,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(&bars.delta_empty[s]);  // every thread: its Delta reads are done
+      if (!kFold) mbar_arrive(&bars.delta_empty[s]);  // every thread: its Delta reads are done
       if (!leader) mbar_arrive(&bars.ds_local);  // the peer's own dQ MMA waits on this
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(L_ds_full);
