@@ -12,10 +12,15 @@ of O after timing (not timed).  Rank 0 prints one JSON line.
 
 Besides the resident step the line carries: the end-to-end step from/to pinned
 host memory (e2e), the Type-1 alpha offload policy (exposed %, split by phase),
-optionally KV streaming (--kv-hot / --device-budget), the bwd kernel's roofline
-object and the oracle's CPU baseline.  Other modes: --parallel cp (sequence
-ring, paper_2503_10377_b200/cp.py), --shard-of G (rank 0's share of a G-GPU
-head split on one GPU), --partition balanced, --impl reference (the oracle).
+optionally KV streaming (--kv-hot / --device-budget, --kv-group G: windows
+shared by G chunks), the bwd kernel's roofline object and the oracle's CPU
+baseline.  Other modes: --parallel cp (sequence ring,
+paper_2503_10377_b200/cp.py), --shard-of G (rank 0's share of a G-GPU head split
+on one GPU), --partition balanced | layer-balanced, --impl reference (the
+oracle), --workload layer (the full GPT layer per chunk, with
+--layer-pool for activation offload that frees device memory and
+--layer-streams 2; its line reports the layer GEMMs' roofline, the Type-1
+offload exposure for sequence-aware vs fixed alpha, and a PP pipeline model).
 
 FLOP convention: 4d per causal pair forward, 10d backward.
 """
