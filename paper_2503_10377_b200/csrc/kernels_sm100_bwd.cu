@@ -74,6 +74,9 @@ constexpr bool kEpiRed = SPPO_EPI_RED;  // dK/dV accumulator epilogue: red.globa
 constexpr uint32_t kOffDQ = kOffDS + kTile;       // kDqBufs x [128 rows][32 fp32] reduce staging
 constexpr uint32_t kOffLSE = kOffDQ + kDqBufs * 16384;  // 2 x 128 fp32 (LSE * log2 e)
 constexpr uint32_t kOffDelta = kOffLSE + 1024;    // 2 x 128 fp32
+#ifndef SPPO_DQ_HINT
+#define SPPO_DQ_HINT 0  // evict_last L2 hint on the dQ reduce-add: measured bwd 1051.7-1052.8 vs 1053.4-1055.3 TF/s, off
+#endif
 #ifndef SPPO_BWD_FOLD
 #define SPPO_BWD_FOLD 0
 #endif
@@ -426,6 +429,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     setmaxnreg_inc<136>();
     // ===================== dQ reducer (TMEM lane = q row) =====================
     const CUtensorMap* mdq = tmap(a, a.dq_slot);
+#if SPPO_DQ_HINT
+    const uint64_t dq_policy = policy_evict_last();  // keep the dQ accumulator lines in L2
+#endif
     const float tau = p.scale;
     const int row = warp * 32 + lane;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
@@ -477,7 +483,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         named_bar_sync(5, 128);
         if (threadIdx.x == 0) {
+#if SPPO_DQ_HINT
+          tma_reduce_add_3d_hint(mdq, stg, pc * 32, head, q0, dq_policy);
+#else
           tma_reduce_add_3d(mdq, stg, pc * 32, head, q0);
+#endif
           bulk_commit();
         }
       }
