@@ -277,6 +277,10 @@ class ChunkedLayer:
         layer has inside one GPU (the attention of chunk i+1 does not depend on
         chunk i's MLP), which fills the tails of each other's launches."""
         strm = stream or torch.cuda.current_stream()
+        with torch.cuda.stream(strm):  # torch-side allocations / copies ordered on strm
+            return self._step(x, dz, strm, mark)
+
+    def _step(self, x, dz, strm, mark):
         self._zero()
         if self.streams < 2 or self.timing:
             for i in range(self.N):
@@ -386,6 +390,10 @@ class ChunkedLayer:
         are overwritten once the D2H completes, proving the backward reads the
         prefetched bytes.  Returns bytes moved per direction."""
         strm = stream or torch.cuda.current_stream()
+        with torch.cuda.stream(strm):  # torch-side allocations / suffix copies ordered on strm
+            return self._step_offload(x, dz, alpha, strm, depth, poison, mark)
+
+    def _step_offload(self, x, dz, alpha, strm, depth, poison, mark):
         self._zero()
         moved = {"d2h": 0, "h2d": 0}
         plan, done = {}, {}
