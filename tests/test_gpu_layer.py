@@ -238,3 +238,26 @@ def test_layer_step_gpt7b_width_matches_oracle(ctx):
     N up to 16384, the CTA-pair kernel over many tiles), full fwd + bwd against
     the fp64 oracle (~5 TFLOP of fp64 on the host: tens of seconds)."""
     _run_and_compare(ctx, 4096, 4096, 32, [0, 2048, 4096], seed=11)
+
+
+def test_layer_pool_offload_on_a_side_stream(ctx):
+    """The step's work (kernels, torch allocations, suffix copies) follows the
+    stream passed in, not torch's current stream."""
+    from paper_2503_10377_b200 import engine_layer, sppo
+    S, H, heads = 2048, 256, 2
+    params, io = _setup(S, H, 12)
+    dev = {k: v.cuda() for k, v in params.items()}
+    off = sppo.partition_equal(S, 4)
+    x, dz = io["x"].cuda(), io["dz"].cuda()
+    ref = engine_layer.ChunkedLayer(ctx, H, heads, off, dev).step(x, dz)
+    ref = {"z": ref["z"].clone(), "dx": ref["dx"].clone()}
+    lay = engine_layer.ChunkedLayer(ctx, H, heads, off, dev, pool=True)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    lay.step_offload(x, dz, [0.5, 0.3, 1.0, 0.0], stream=side)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    assert torch.equal(lay.z, ref["z"])
+    rel = (lay.dx.double() - ref["dx"].double()).norm() / ref["dx"].double().norm()
+    assert rel < 1e-4
+    lay.free_host()
