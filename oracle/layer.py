@@ -225,3 +225,40 @@ def layer_flops(S, H, offsets_pairs=None, d=128):
     heads = H // d
     gemm = 24 * H * H * S
     return dict(gemm_fwd=gemm, gemm_bwd=2 * gemm, attn_fwd=4 * d * heads * pairs, attn_bwd=10 * d * heads * pairs)
+
+
+def sampled_rows_fwd(x, params, heads, rows, block=16384):
+    """Layer output z at the token rows `rows` only, for sequences too long for
+    layer_fwd: LN1 and the K / V projections of every token (in row blocks),
+    then for each sampled row its query, causal attention over keys 0..p (the
+    definition, oracle/attention.py), out-projection, LN2 and MLP.  Pinned
+    against layer_fwd on small inputs (tests/test_layer_oracle.py)."""
+    p = _f64params(params)
+    x = np.asarray(x, np.float64)
+    S, H = x.shape
+    d = H // heads
+    rows = sorted(int(r) for r in rows)
+    last = rows[-1] + 1
+    wq, wk, wv = p["w_qkv"][:H], p["w_qkv"][H:2 * H], p["w_qkv"][2 * H:]
+    bq, bk, bv = p["b_qkv"][:H], p["b_qkv"][H:2 * H], p["b_qkv"][2 * H:]
+    k = np.empty((last, H))
+    v = np.empty((last, H))
+    for a0 in range(0, last, block):
+        a1 = min(last, a0 + block)
+        a, _, _ = layernorm_fwd(x[a0:a1], p["ln1_g"], p["ln1_b"])
+        k[a0:a1] = a @ wk.T + bk
+        v[a0:a1] = a @ wv.T + bv
+    tau = 1.0 / np.sqrt(d)
+    out = np.empty((len(rows), H))
+    for n, r in enumerate(rows):
+        a, _, _ = layernorm_fwd(x[r:r + 1], p["ln1_g"], p["ln1_b"])
+        q = (a @ wq.T + bq)[0]
+        o = np.empty(H)
+        for h in range(heads):
+            sl = slice(h * d, (h + 1) * d)
+            s = tau * (k[:r + 1, sl] @ q[sl])
+            w = np.exp(s - s.max())
+            o[sl] = (w / w.sum()) @ v[:r + 1, sl]
+        z, _ = _chunk_fwd_post(x[r:r + 1], o[None, :], p)
+        out[n] = z[0]
+    return rows, out

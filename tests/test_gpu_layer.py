@@ -261,3 +261,27 @@ def test_layer_pool_offload_on_a_side_stream(ctx):
     rel = (lay.dx.double() - ref["dx"].double()).norm() / ref["dx"].double().norm()
     assert rel < 1e-4
     lay.free_host()
+
+
+@pytest.mark.slow
+def test_layer_full_bench_shape_sampled_rows(ctx):
+    """The bench's layer workload at full size — GPT-7B layer, S = 128K, N = 16,
+    the resident step bench.py times — checked on sampled output rows (every
+    chunk boundary c-1 / c, first and last rows) against the fp64 oracle's
+    sampled-row forward (K / V of all tokens, then causal attention per row)."""
+    from paper_2503_10377_b200 import engine_layer, sppo
+    S, H, heads, N = 131072, 4096, 32, 16
+    params = synth.make_layer_params(H, 0)
+    io = synth.make_layer_io(S, H, 0)
+    off = sppo.partition_equal(S, N)
+    lay = engine_layer.ChunkedLayer(ctx, H, heads, off, {k: v.cuda() for k, v in params.items()})
+    out = lay.step(io["x"].cuda(), io["dz"].cuda())
+    torch.cuda.synchronize()
+    rows = sorted({0, 1, S - 1} | {c - 1 for c in off[1:-1]} | set(off[1:-1]))
+    z_gpu = out["z"][rows].double().cpu().numpy()
+    p64 = {k: v.double().numpy() for k, v in params.items()}
+    rows, z_ref = L.sampled_rows_fwd(io["x"].double().numpy(), p64, heads, rows)
+    rms = np.sqrt(np.mean(z_ref ** 2))
+    rel = np.linalg.norm(z_gpu - z_ref) / np.linalg.norm(z_ref)
+    assert rel <= 1e-2, rel
+    assert (np.abs(z_gpu - z_ref) <= 5e-2 * np.abs(z_ref) + 5e-2 * rms).all()

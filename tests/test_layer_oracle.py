@@ -139,3 +139,12 @@ def test_layer_flops_counts():
     f = L.layer_flops(1024, 256, d=64)
     assert f["gemm_fwd"] == 2 * (3 * 256 * 256 + 256 * 256 + 2 * 4 * 256 * 256) * 1024
     assert f["attn_fwd"] == 4 * 64 * 4 * 1024 * 1025 // 2
+
+
+def test_sampled_rows_fwd_equals_dense():
+    S, H, heads = 40, 16, 2
+    p = _params(H, seed=13)
+    io = _io(S, H, seed=13)
+    z, _ = L.layer_fwd(io["x"], p, heads)
+    rows, zs = L.sampled_rows_fwd(io["x"], p, heads, [0, 7, 8, 23, 39], block=16)
+    np.testing.assert_allclose(zs, z[rows], rtol=1e-12, atol=1e-12)
