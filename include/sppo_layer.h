@@ -103,7 +103,7 @@ sppo_status sppo_layernorm_bwd(sppo_ctx ctx, const void* dy, const void* x, cons
  *   prod_acc[c] += sum_r dy[r][c] (x[r][c] - mean_r) rstd_r      (if x != NULL)
  *   dy is split along columns into `parts` equal bf16 buffers dy[0..parts-1]
  *   (total width cols); x bf16 [rows][cols]; sum_acc, prod_acc fp32 [cols].
- *   cols / parts % 256 == 0.  Accumulation order across rows is not fixed
+ *   cols / parts % 8 == 0.  Accumulation order across rows is not fixed
  *   (fp32 atomics): results are reproducible to fp32 rounding only.
  */
 sppo_status sppo_col_reduce(sppo_ctx ctx, int32_t parts, const void* const* dy, const void* x, const float* mean,

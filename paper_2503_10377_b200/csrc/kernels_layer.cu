@@ -128,8 +128,9 @@ struct ColParts {
   const __nv_bfloat16* p[3];
 };
 
-// grid (cols / 256, splits): CTA (cb, s) reduces columns [256 cb, 256 cb + 256)
-// over rows [s * rows_per, (s + 1) * rows_per).
+// grid (ceil(cols / 256), splits): CTA (cb, s) reduces columns [256 cb, 256 cb + 256)
+// (clipped to cols) over rows [s * rows_per, (s + 1) * rows_per); a lane owns 8
+// consecutive columns, which lie in one part (part widths are multiples of 8).
 __global__ void __launch_bounds__(256) col_reduce_kernel(ColParts dy, int part_w, const __nv_bfloat16* __restrict__ x,
                                                          const float* __restrict__ mean,
                                                          const float* __restrict__ rstd, int64_t rows, int cols,
@@ -138,21 +139,23 @@ __global__ void __launch_bounds__(256) col_reduce_kernel(ColParts dy, int part_w
   __shared__ float red[2][kRowsPerCta][256];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c0 = blockIdx.x * 256;
-  const int part = c0 / part_w;
-  const int pc = c0 - part * part_w + lane * 8;
+  const int col = c0 + lane * 8;          // this lane's 8 columns (parts are multiples of 8 wide)
+  const bool live = col < cols;
+  const int part = live ? col / part_w : 0;
+  const int pc = col - part * part_w;
   const __nv_bfloat16* src = dy.p[part];
   const int64_t r0 = (int64_t)blockIdx.y * rows_per;
   const int64_t r1 = r0 + rows_per < rows ? r0 + rows_per : rows;
   float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   float q[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int64_t r = r0 + w; r < r1; r += kRowsPerCta) {
+  for (int64_t r = r0 + w; live && r < r1; r += kRowsPerCta) {
     float d[8];
     ld8(src + r * part_w + pc, d);
 #pragma unroll
     for (int e = 0; e < 8; ++e) s[e] += d[e];
     if (x) {
       float v[8];
-      ld8(x + r * cols + c0 + lane * 8, v);
+      ld8(x + r * cols + col, v);
       const float mu = mean[r], rs = rstd[r];
 #pragma unroll
       for (int e = 0; e < 8; ++e) q[e] += d[e] * (v[e] - mu) * rs;
@@ -171,8 +174,10 @@ __global__ void __launch_bounds__(256) col_reduce_kernel(ColParts dy, int part_w
     ts += red[0][k][c];
     tq += red[1][k][c];
   }
-  atomicAdd(sum_acc + c0 + c, ts);
-  if (x) atomicAdd(prod_acc + c0 + c, tq);
+  if (c0 + c < cols) {
+    atomicAdd(sum_acc + c0 + c, ts);
+    if (x) atomicAdd(prod_acc + c0 + c, tq);
+  }
 }
 
 }  // namespace
@@ -205,7 +210,7 @@ cudaError_t launch_col_reduce(int parts, const void* const* dy, const void* x, c
   if (rows == 0) return cudaSuccess;
   ColParts cp{};
   for (int i = 0; i < parts; ++i) cp.p[i] = static_cast<const __nv_bfloat16*>(dy[i]);
-  const int cblocks = cols / 256;
+  const int cblocks = (cols + 255) / 256;
   int64_t splits = (4LL * num_sms + cblocks - 1) / cblocks;
   const int64_t max_splits = (rows + 4 * kRowsPerCta - 1) / (4 * kRowsPerCta);  // >= 4 rows per warp
   if (splits > max_splits) splits = max_splits;

@@ -172,8 +172,8 @@ sppo_status sppo_col_reduce(sppo_ctx ctx, int32_t parts, const void* const* dy, 
                             void* stream) {
   if (!ctx || !dy || !sum_acc) return err(SPPO_E_ARG, "col_reduce: NULL argument");
   if (parts < 1 || parts > 3) return err(SPPO_E_ARG, "col_reduce: parts must be in 1..3");
-  if (rows < 0 || cols < 256 || cols % parts || (cols / parts) % 256)
-    return err(SPPO_E_SHAPE, "col_reduce: cols / parts must be a multiple of 256 (cols = %d)", cols);
+  if (rows < 0 || cols < 8 || cols % parts || (cols / parts) % 8)
+    return err(SPPO_E_SHAPE, "col_reduce: cols / parts must be a multiple of 8 (cols = %d)", cols);
   if (x && (!mean || !rstd || !prod_acc)) return err(SPPO_E_ARG, "col_reduce: x needs mean, rstd, prod_acc");
   for (int i = 0; i < parts; ++i)
     if (!dy[i] || !al16(dy[i])) return err(SPPO_E_ALIGN, "col_reduce: dy part NULL or not 16-byte aligned");

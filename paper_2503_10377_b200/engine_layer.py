@@ -51,13 +51,41 @@ STATS = ("lse", "mu1", "rstd1", "mu2", "rstd2")  # fp32 statistics, offloaded wh
 LN_EPS = 1e-5
 
 
+def shard_params(params: dict, hidden: int, heads: int, rank: int, size: int) -> dict:
+    """Rank `rank`'s tensor-parallel shard of a layer's parameters (Megatron
+    layout): W_qkv / b_qkv rows of this rank's heads (q, k and v parts), W_1 /
+    b_1 rows (column-parallel), W_o / W_2 columns (row-parallel); LayerNorm
+    parameters, b_o and b_2 replicated.  Contiguous copies (GEMM operands)."""
+    H, Hl = hidden, hidden // size
+    r = slice(rank * Hl, (rank + 1) * Hl)
+    f = slice(rank * 4 * Hl, (rank + 1) * 4 * Hl)
+    out = dict(params)
+    out["w_qkv"] = torch.cat([params["w_qkv"][k * H:(k + 1) * H][r] for k in range(3)]).contiguous()
+    out["b_qkv"] = torch.cat([params["b_qkv"][k * H:(k + 1) * H][r] for k in range(3)]).contiguous()
+    out["w_o"] = params["w_o"][:, r].contiguous()
+    out["w_1"] = params["w_1"][f].contiguous()
+    out["b_1"] = params["b_1"][f].contiguous()
+    out["w_2"] = params["w_2"][:, f].contiguous()
+    return out
+
+
 class ChunkedLayer:
     def __init__(self, ctx: sppo.Context, hidden: int, heads: int, offsets, params: dict, device="cuda",
-                 timing: bool = False, pool: bool = False, streams: int = 1):
+                 timing: bool = False, pool: bool = False, streams: int = 1, tp=None):
+        """tp = (rank, size, process group or None): Megatron-style tensor
+        parallelism over the heads (P:157 [§2]; the north star's "heads are
+        partitioned across the GPUs"): `params` are this rank's shard
+        (shard_params), the QKV / fc1 projections are column-parallel, out-proj /
+        fc2 row-parallel, and their partial sums (plus the backward's partial
+        LayerNorm inputs) are all-reduced — the layer's real exchange steps."""
         self.ctx = ctx
-        self.H, self.heads = hidden, heads
+        self.tp_rank, self.tp_size, self.tp_group = tp if tp is not None else (0, 1, None)
+        if heads % self.tp_size:
+            raise ValueError("heads must divide over the tensor-parallel ranks")
+        self.H, self.heads = hidden, heads // self.tp_size  # self.heads: heads on this rank
         self.d = hidden // heads
-        self.L = sppo.Layout(heads, self.d, offsets, dtype=sppo.SPPO_BF16)
+        self.Hl = self.heads * self.d  # width of this rank's q / k / v / o
+        self.L = sppo.Layout(self.heads, self.d, offsets, dtype=sppo.SPPO_BF16)
         self.N = self.L.num_chunks
         if self.N > 256:
             raise ValueError("ChunkedLayer issues one attention window per chunk: N <= 256")
@@ -66,32 +94,35 @@ class ChunkedLayer:
         self.p = params
         self.timing = timing
         self.pool = pool
-        H = hidden
+        H, Hl = hidden, self.Hl
         bf = dict(dtype=torch.bfloat16, device=self.device)
         f32 = dict(dtype=torch.float32, device=self.device)
         # Type-0 (resident) and outputs: whole sequence, token-major
-        self.k = torch.empty((S, H), **bf)
-        self.v = torch.empty((S, H), **bf)
+        self.k = torch.empty((S, Hl), **bf)
+        self.v = torch.empty((S, Hl), **bf)
         self.z = torch.empty((S, H), **bf)
         self.dx = torch.empty((S, H), **bf)
-        self.dk_acc = torch.empty((S, H), **f32)
-        self.dv_acc = torch.empty((S, H), **f32)
+        self.dk_acc = torch.empty((S, Hl), **f32)
+        self.dv_acc = torch.empty((S, Hl), **f32)
         # per-chunk backward scratch (longest chunk)
         smax = max(self.L.chunk_len(i) for i in range(self.N))
-        self.du = torch.empty((smax, 4 * H), **bf)
-        for n in ("dbn", "da", "dq", "dkc", "dvc"):
+        self.du = torch.empty((smax, 4 * Hl), **bf)
+        for n in ("dbn", "da"):
             setattr(self, n, torch.empty((smax, H), **bf))
+        for n in ("dq", "dkc", "dvc"):
+            setattr(self, n, torch.empty((smax, Hl), **bf))
         # d_o and dy pass from backward_b(i) to backward_a(i): two sets, so that
         # backward_b(i-1) on a second stream can run while backward_a(i) reads them
         self.dy2 = [torch.empty((smax, H), **bf) for _ in range(2)]
-        self.d_o2 = [torch.empty((smax, H), **bf) for _ in range(2)]
-        self.dq_acc = torch.empty((smax, H), **f32)
-        self.delta = torch.empty((smax * heads,), **f32)
+        self.d_o2 = [torch.empty((smax, Hl), **bf) for _ in range(2)]
+        self.dq_acc = torch.empty((smax, Hl), **f32)
+        self.delta = torch.empty((smax * self.heads,), **f32)
         # Type-1: whole-sequence buffers (resident) or per-chunk allocations (pool)
         self._full = None
         if not pool:
-            self._full = {n: torch.empty((S, 4 * H if n in ("u", "g") else H), **bf) for n in TYPE1}
-            self._full.update({n: torch.empty((S * (heads if n == "lse" else 1),), **f32) for n in STATS})
+            self._full = {n: torch.empty((S,) + self._t1_shape(n, 1)[0][1:], dtype=self._t1_shape(n, 1)[1],
+                                         device=self.device) for n in TYPE1}
+            self._full.update({n: torch.empty((S * (self.heads if n == "lse" else 1),), **f32) for n in STATS})
         self.T = [None] * self.N
         self.grads = {n: torch.zeros(tuple(params[n].shape), **f32) for n in PARAM_NAMES}
         self.launches = 0
@@ -109,8 +140,10 @@ class ChunkedLayer:
 
     def _t1_shape(self, name, s):
         if name in ("u", "g"):
-            return (s, 4 * self.H), torch.bfloat16
-        if name in TYPE1:
+            return (s, 4 * self.Hl), torch.bfloat16
+        if name in ("q", "o"):
+            return (s, self.Hl), torch.bfloat16
+        if name in TYPE1:  # a, y, b: LayerNorm inputs / outputs, full width on every rank
             return (s, self.H), torch.bfloat16
         return ((s * self.heads,) if name == "lse" else (s,)), torch.float32
 
@@ -137,6 +170,22 @@ class ChunkedLayer:
             e1.record(kw["stream"])
             ev.append((e0, e1, 2 * M * N * K))
         self.launches += 1
+
+    def _allreduce(self, t, strm):
+        """Sum over the tensor-parallel ranks, in place (no-op without TP).  NCCL:
+        stream-ordered on `strm` (the current stream inside step); otherwise
+        (gloo, tests) host-staged."""
+        if self.tp_size == 1:
+            return
+        import torch.distributed as dist
+        st = strm if isinstance(strm, torch.cuda.Stream) else torch.cuda.current_stream()
+        with torch.cuda.stream(st):
+            if dist.get_backend(self.tp_group) == "nccl":
+                dist.all_reduce(t, group=self.tp_group)
+            else:
+                h = t.float().cpu()
+                dist.all_reduce(h, group=self.tp_group)
+                t.copy_(h)
 
     def _attn_ev(self, strm):
         if self.attn_events is None:
@@ -176,7 +225,7 @@ class ChunkedLayer:
         T = self.T[i] = self._t1_set(i)
         xi = self.rows(x, i)
         self.ctx.layernorm_fwd(xi, p["ln1_g"], p["ln1_b"], T["a"], T["mu1"], T["rstd1"], eps=LN_EPS, stream=strm)
-        self._gemm(s, 3 * H, H, T["a"], p["w_qkv"], [T["q"], self.rows(self.k, i), self.rows(self.v, i)],
+        self._gemm(s, 3 * self.Hl, H, T["a"], p["w_qkv"], [T["q"], self.rows(self.k, i), self.rows(self.v, i)],
                    bias=p["b_qkv"], stream=strm)
         ids, ks, vs = self._kv(i)
         ae = self._attn_ev(strm)
@@ -189,13 +238,19 @@ class ChunkedLayer:
         """Out-projection + residual, LN2, MLP of chunk i (needs only forward_a(i))."""
         p, H, s = self.p, self.H, self.L.chunk_len(i)
         T = self.T[i]
-        self._gemm(s, H, H, T["o"], p["w_o"], T["y"], bias=p["b_o"], residual=self.rows(x, i), stream=strm)
+        Hl, r0 = self.Hl, self.tp_rank == 0
+        # row-parallel out-proj: partial sums over the local heads; the bias and the
+        # residual enter once (rank 0), then the all-reduce sums the ranks' partials
+        self._gemm(s, H, Hl, T["o"], p["w_o"], T["y"], bias=p["b_o"] if r0 else None,
+                   residual=self.rows(x, i) if r0 else None, stream=strm)
+        self._allreduce(T["y"], strm)
         self.ctx.layernorm_fwd(T["y"], p["ln2_g"], p["ln2_b"], T["b"], T["mu2"], T["rstd2"], eps=LN_EPS,
                                stream=strm)
-        self._gemm(s, 4 * H, H, T["b"], p["w_1"], T["g"], bias=p["b_1"], aux_out=T["u"],
+        self._gemm(s, 4 * Hl, H, T["b"], p["w_1"], T["g"], bias=p["b_1"], aux_out=T["u"],
                    epilogue=sppo.SPPO_EPI_GELU, stream=strm)
-        self._gemm(s, H, 4 * H, T["g"], p["w_2"], self.rows(self.z, i), bias=p["b_2"], residual=T["y"],
-                   stream=strm)
+        self._gemm(s, H, 4 * Hl, T["g"], p["w_2"], self.rows(self.z, i), bias=p["b_2"] if r0 else None,
+                   residual=T["y"] if r0 else None, stream=strm)
+        self._allreduce(self.rows(self.z, i), strm)
         self.launches += 1
 
     # ------------------------------------------------------------------ backward of chunk i
@@ -217,19 +272,22 @@ class ChunkedLayer:
         dzi = self.rows(dz, i)
         acc = sppo.SPPO_EPI_ACC_F32
         # MLP: fc2 then fc1
-        self._gemm(s, 4 * H, H, dzi, p["w_2"], du, b_mn=1, aux_in=T["u"], epilogue=sppo.SPPO_EPI_DGELU, stream=strm)
-        self._gemm(H, 4 * H, s, dzi, T["g"], gr["w_2"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
+        Hl = self.Hl
+        self._gemm(s, 4 * Hl, H, dzi, p["w_2"], du, b_mn=1, aux_in=T["u"], epilogue=sppo.SPPO_EPI_DGELU,
+                   stream=strm)
+        self._gemm(H, 4 * Hl, s, dzi, T["g"], gr["w_2"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
         ctx.col_reduce(dzi, s, H, gr["b_2"], stream=strm)
-        self._gemm(s, H, 4 * H, du, p["w_1"], dbn, b_mn=1, stream=strm)
-        self._gemm(4 * H, H, s, du, T["b"], gr["w_1"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
-        ctx.col_reduce(du, s, 4 * H, gr["b_1"], stream=strm)
+        self._gemm(s, H, 4 * Hl, du, p["w_1"], dbn, b_mn=1, stream=strm)
+        self._allreduce(dbn, strm)  # the LN2 input gradient sums the ranks' column-parallel fc1 parts
+        self._gemm(4 * Hl, H, s, du, T["b"], gr["w_1"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
+        ctx.col_reduce(du, s, 4 * Hl, gr["b_1"], stream=strm)
         # LN2 (+ residual stream gradient dz)
         ctx.layernorm_bwd(dbn, T["y"], p["ln2_g"], T["mu2"], T["rstd2"], dy, dres=dzi, stream=strm)
         ctx.col_reduce(dbn, s, H, gr["ln2_b"], x=T["y"], mean=T["mu2"], rstd=T["rstd2"], prod_acc=gr["ln2_g"],
                        stream=strm)
         # out-proj
-        self._gemm(s, H, H, dy, p["w_o"], d_o, b_mn=1, stream=strm)
-        self._gemm(H, H, s, dy, T["o"], gr["w_o"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
+        self._gemm(s, Hl, H, dy, p["w_o"], d_o, b_mn=1, stream=strm)
+        self._gemm(H, Hl, s, dy, T["o"], gr["w_o"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
         ctx.col_reduce(dy, s, H, gr["b_o"], stream=strm)
         self.launches += 5
 
@@ -252,9 +310,11 @@ class ChunkedLayer:
         if ae is not None:
             ae.record(strm)
         # QKV projection from the three gradient parts, then LN1 (+ dy)
-        self._gemm(s, H, 3 * H, [dq, dk, dv], p["w_qkv"], da, b_mn=1, stream=strm)
-        self._gemm(3 * H, H, s, [dq, dk, dv], T["a"], gr["w_qkv"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
-        ctx.col_reduce([dq, dk, dv], s, 3 * H, gr["b_qkv"], stream=strm)
+        Hl = self.Hl
+        self._gemm(s, H, 3 * Hl, [dq, dk, dv], p["w_qkv"], da, b_mn=1, stream=strm)
+        self._allreduce(da, strm)  # the LN1 input gradient sums the ranks' column-parallel QKV parts
+        self._gemm(3 * Hl, H, s, [dq, dk, dv], T["a"], gr["w_qkv"], a_mn=1, b_mn=1, epilogue=acc, stream=strm)
+        ctx.col_reduce([dq, dk, dv], s, 3 * Hl, gr["b_qkv"], stream=strm)
         ctx.layernorm_bwd(da, xi, p["ln1_g"], T["mu1"], T["rstd1"], self.rows(self.dx, i), dres=dy, stream=strm)
         ctx.col_reduce(da, s, H, gr["ln1_b"], x=xi, mean=T["mu1"], rstd=T["rstd1"], prod_acc=gr["ln1_g"],
                        stream=strm)

@@ -163,3 +163,17 @@ def test_col_reduce_split_parts(ctx):
     ctx.col_reduce([p.cuda() for p in parts], rows, 3 * H, acc)
     ref = 1 + np.concatenate([_np(p).sum(axis=0) for p in parts])
     _close(acc, ref, rtol=1e-4, ftol=1e-5, what="bias grad over 3 parts")
+
+
+def test_col_reduce_narrow_parts_and_ragged_width(ctx):
+    """Parts of 128 columns (a tensor-parallel QKV gradient) and widths that are not
+    a multiple of 256."""
+    rows = 300
+    parts = [_rand((rows, 128), 50 + i) for i in range(3)]
+    acc = torch.zeros(384, device="cuda")
+    ctx.col_reduce([p.cuda() for p in parts], rows, 384, acc)
+    _close(acc, np.concatenate([_np(p).sum(axis=0) for p in parts]), rtol=1e-4, ftol=1e-5, what="3 x 128")
+    x = _rand((rows, 136), 60)
+    acc = torch.zeros(136, device="cuda")
+    ctx.col_reduce(x.cuda(), rows, 136, acc)
+    _close(acc, _np(x).sum(axis=0), rtol=1e-4, ftol=1e-5, what="width 136")
