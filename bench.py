@@ -539,8 +539,9 @@ def layer_offsets(args, S, N, H):
 def run_layer(args, cfg, ws, rank, local):
     """One step = the GPT layer (hidden = heads*d of the config) forward over the
     N chunks then backward in reverse (engine_layer.ChunkedLayer).  N > 1 ranks
-    run independent replicas (weak scaling; no collective: the layer has no
-    data-parallel exchange inside the step)."""
+    partition the heads (tensor parallelism: column / row-parallel projections,
+    NCCL all-reduce of the partial sums, engine_layer tp=...): the total work is
+    fixed (strong scaling), value = the whole layer's FLOPs / max-over-ranks time."""
     from paper_2503_10377_b200 import engine_layer, sppo
     import synth
 
@@ -551,8 +552,11 @@ def run_layer(args, cfg, ws, rank, local):
     ctx = sppo.Context(local)
     offsets = layer_offsets(args, S, N, H)
     params = synth.make_layer_params(H, 0, device=dev)
+    if ws > 1:
+        params = engine_layer.shard_params(params, H, heads, rank, ws)
     io = synth.make_layer_io(S, H, 0, device=dev)
-    lay = engine_layer.ChunkedLayer(ctx, H, heads, offsets, params, device=dev, streams=args.layer_streams)
+    lay = engine_layer.ChunkedLayer(ctx, H, heads, offsets, params, device=dev, streams=args.layer_streams,
+                                    tp=(rank, ws, None) if ws > 1 else None)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         lay.step(io["x"], io["dz"], stream)
@@ -666,7 +670,7 @@ def run_layer(args, cfg, ws, rank, local):
             if rep > 0:
                 res.append(e0.elapsed_time(e1))
         e2e_ms = max_over_ranks(statistics.median(res), ws)
-        e2e = {"value": round(fl * ws / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s", "ms_per_step": round(e2e_ms, 3),
+        e2e = {"value": round(fl / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s", "ms_per_step": round(e2e_ms, 3),
                "h2d_bytes_per_step": h2d * ws, "d2h_bytes_per_step": d2h * ws,
                "path": "pinned host x (forward order), dz (backward order) -> chunk-wise sppo_kv_prefetch overlapped "
                        "with compute; z after fwd(i), dx after bwd(i) -> sppo_kv_offload"}
@@ -679,20 +683,20 @@ def run_layer(args, cfg, ws, rank, local):
         cpu = {"value": round(c["value"], 6), "unit": "TFLOP/s", "cores": c["cores"], "kind": "oracle",
                "sample": c["sample"]}
     gemm_tf = gemm_fl / (gemm_ms * 1e-3) / 1e12
-    line = {"metric": LAYER_METRIC, "value": round(tflops * ws, 2), "unit": "TFLOP/s", "n_gpus": ws,
+    line = {"metric": LAYER_METRIC, "value": round(tflops, 2), "unit": "TFLOP/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": cfg["workload"].replace("attention layer", "layer") + " -- full GPT layer "
                                    f"(hidden {H}, MLP 4x, LayerNorm, GELU) per chunk",
                        "hidden": H, "heads": heads, "seq_len": S, "chunks": N, "partition": args.partition,
                        "streams": args.layer_streams,
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "parallelism": f"tensor parallel: heads over {ws} GPUs" if ws > 1 else "single GPU",
                        "l2": "inputs larger than L2 (activations GBs per step)"},
-            "tokens_per_s": round(S * ws / (ms * 1e-3), 1), "pct_of_bf16_peak": round(100 * tflops / peaks["burst"], 2),
+            "tokens_per_s": round(S / (ms * 1e-3), 1), "pct_of_bf16_peak": round(100 * tflops / ws / peaks["burst"], 2),
             "fwd_tflops": round(f_fwd / (fwd_ms * 1e-3) / 1e12, 1), "bwd_tflops": round(f_bwd / (bwd_ms * 1e-3) / 1e12, 1),
             "breakdown": {"gemm_ms": round(gemm_ms, 3), "gemm_tflops": round(gemm_tf, 1),
                           "attention_ms": round(attn_ms, 3),
-                          "attention_tflops": round((f_attn_fwd * 3.5) / (attn_ms * 1e-3) / 1e12, 1),
+                          "attention_tflops": round((f_attn_fwd * 3.5) / ws / (attn_ms * 1e-3) / 1e12, 1),
                           "gemm_flop_share": round(3 * f_gemm_fwd / fl, 3)},
             "gpu_launches": launches,
             "roofline": {"bound": "tensor", "kernel": "gemm_kernel (all layer GEMMs, event-timed in one step)",
