@@ -154,7 +154,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int q_tiles = (p.q_len + BQ - 1) / BQ;
   const int qt_first = max(0, (a.start[c] + pair_row0 - p.q_start) / BQ);
   const int M = q_tiles - qt_first;
-  const int rot = (int)(((uint32_t)pair * 7u + blockIdx.y * 13u) % (uint32_t)M);  // spread dQ reduce traffic
+#ifndef SPPO_BWD_ROT
+#define SPPO_BWD_ROT 1  // measured: without the rotation bwd 985.6-986.0 vs 1042.0-1049.1 TF/s
+#endif
+  // start Q tile rotated per pair: concurrent pairs reduce dQ into different rows
+  const int rot = SPPO_BWD_ROT ? (int)(((uint32_t)pair * 7u + blockIdx.y * 13u) % (uint32_t)M) : 0;
   auto qtile = [&](int m) { return qt_first + (m + rot) % M; };
 
   if (threadIdx.x == 0) {
