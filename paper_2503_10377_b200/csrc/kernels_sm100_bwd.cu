@@ -158,7 +158,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #define SPPO_BWD_ROT 1  // measured: without the rotation bwd 985.6-986.0 vs 1042.0-1049.1 TF/s
 #endif
   // start Q tile rotated per pair: concurrent pairs reduce dQ into different rows
-  const int rot = SPPO_BWD_ROT ? (int)(((uint32_t)pair * 7u + blockIdx.y * 13u) % (uint32_t)M) : 0;
+#ifndef SPPO_BWD_ROT_SHIFT
+#define SPPO_BWD_ROT_SHIFT 0  // 2^shift consecutive pairs share a start tile (reduce the same dQ lines together)
+#endif
+  const int rot = SPPO_BWD_ROT ? (int)((((uint32_t)pair >> SPPO_BWD_ROT_SHIFT) * 7u + blockIdx.y * 13u) % (uint32_t)M)
+                               : 0;
   auto qtile = [&](int m) { return qt_first + (m + rot) % M; };
 
   if (threadIdx.x == 0) {
