@@ -114,6 +114,9 @@ class ClockSampler:
                 "samples": len(sm), "power_w_max": max(float(r[3]) for r in rows if r[3].strip()[:1].isdigit())}
 
 
+CLOCK_REJECT = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
 def flops_of(offsets, heads, d, part="fwd+bwd"):
     from paper_2503_10377_b200 import sppo
     pairs = sppo.causal_pairs(offsets)  # product's own host helper (a0 / FLOP accounting)
@@ -215,23 +218,32 @@ def run_ours(args, cfg, ws, rank, local):
     torch.cuda.synchronize()
     eng.events = {"fwd": [], "bwd": []}
     eng.timing = False  # per-call events are not used for the timed steps (phase marks are)
-    phase = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    eng.launches = 0
-    barrier(ws)
-    torch.cuda.synchronize()
-    clk = ClockSampler(local)
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    t0.record(stream)
-    for st in range(args.steps):
-        marks[st].record(stream)  # step start; eng.step records the fwd/bwd boundary in phase[st]
-        eng.step(x["q"], x["k"], x["v"], x["do"], stream, mark=phase[st])
-    marks[args.steps].record(stream)
-    t1.record(stream)
-    torch.cuda.synchronize()
-    clocks = clk.stop()
-    barrier(ws)
+    remeasured = None
+    for attempt in range(2):
+        phase = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        eng.launches = 0
+        barrier(ws)
+        torch.cuda.synchronize()
+        clk = ClockSampler(local)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        t0.record(stream)
+        for st in range(args.steps):
+            marks[st].record(stream)  # step start; eng.step records the fwd/bwd boundary in phase[st]
+            eng.step(x["q"], x["k"], x["v"], x["do"], stream, mark=phase[st])
+        marks[args.steps].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        clocks = clk.stop()
+        barrier(ws)
+        # timing rules: a run that saw a hardware / thermal slowdown is re-measured once
+        bad = sorted(set((clocks or {}).get("reasons", [])) & CLOCK_REJECT)
+        if not bad or attempt == 1:
+            break
+        remeasured = {"first_attempt_reasons": bad, "first_attempt_ms_per_step": t0.elapsed_time(t1) / args.steps}
+    if clocks is not None and remeasured is not None:
+        clocks["remeasured"] = remeasured
     ms_local = t0.elapsed_time(t1) / args.steps
     ms = max_over_ranks(ms_local, ws)
     launches = eng.launches // args.steps
