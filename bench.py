@@ -175,6 +175,34 @@ def dist_setup():
     return ws, rank, local
 
 
+def bind_numa(local):
+    """P:472 [§7] "bind the NUMA node": pin this rank's host threads to the CPUs of
+    its GPU's NUMA node (sysfs), so the offload copies' host side and the pinned
+    arena (sppo_host_alloc, NUMA-local) sit on the same socket.  Returns a dict
+    for the JSON line."""
+    if not torch.cuda.is_available():
+        return None
+    try:
+        p = torch.cuda.get_device_properties(local)
+        bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        node = int(open(f"/sys/bus/pci/devices/{bus}/numa_node").read().strip())
+    except Exception as e:
+        return {"node": None, "note": f"NUMA node unknown ({type(e).__name__})"}
+    if node < 0:
+        return {"node": node, "note": "GPU reports no NUMA affinity (single-node host)"}
+    try:
+        cpus = set()
+        for part in open(f"/sys/devices/system/node/node{node}/cpulist").read().strip().split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0) or cpus
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        return {"node": node, "cpus": len(cpus)}
+    except Exception as e:
+        return {"node": node, "note": f"affinity not set ({type(e).__name__})"}
+
+
 def head_range(heads, ws, rank):
     from paper_2503_10377_b200.dist import head_range as hr
     return hr(heads, ws, rank)
@@ -398,6 +426,7 @@ def run_ours(args, cfg, ws, rank, local):
 
     # ---- final gather of O over NCCL (multi-GPU only, not timed in value)
     gather = None
+    full = eng.o
     if ws > 1:
         from paper_2503_10377_b200.dist import gather_heads
         g0 = time.perf_counter()
@@ -406,6 +435,10 @@ def run_ours(args, cfg, ws, rank, local):
         import torch.distributed as dist
         gather = {"op": f"all_gather O over {dist.get_backend()}", "ms": round((time.perf_counter() - g0) * 1e3, 2),
                   "bytes": full.numel() * full.element_size()}
+    o_digest = None
+    if args.o_digest:  # forward is bitwise deterministic per head: sharded and unsharded runs must agree
+        import hashlib
+        o_digest = hashlib.sha256(full.contiguous().view(torch.uint8).cpu().numpy().tobytes()).hexdigest()
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -441,10 +474,65 @@ def run_ours(args, cfg, ws, rank, local):
                      "peak_kind": "sustained bf16 (kernel timed inside a long step), " + peaks["source"],
                      "share_of_step": round(bwd_ms / ms, 3)},
         "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "offload": offload, "kv_stream": kvs,
-        "gather": gather,
+        "gather": gather, "numa": args.numa,
         "cpu_baseline": cpu,
     }
+    if o_digest:
+        line["o_sha256"] = o_digest
+    if (args.config == "C2" and ws == 1 and args.shard_of == 1 and not args.no_c3 and args.partition == "equal"
+            and not (args.heads or args.seq_len or args.chunks)):
+        # the north-star target workload (1M tokens on 1 GPU) on the same clock as the line
+        del eng, x, full
+        torch.cuda.empty_cache()
+        line["target_c3"] = resident_sub("C3", local)
     return line
+
+
+def resident_sub(name, local, steps=2, warmup=1):
+    """Bounded resident fwd+bwd measurement of another config on this GPU (BASELINE.json
+    north_star target: >= 60 % of dense bf16 peak at 1M tokens on 1 GPU): `warmup`
+    untimed steps (each ~30 s at C3), `steps` timed with CUDA events on the launching
+    stream, clocks sampled during the timed region."""
+    from paper_2503_10377_b200 import engine, sppo
+    from synth import make_tensor
+    cfg = CONFIGS[name]
+    dev = torch.device("cuda", local)
+    heads = list(range(cfg["heads"]))
+    h, d, S, N = len(heads), cfg["d"], cfg["S"], cfg["N"]
+    ctx = sppo.Context(local)
+    offsets = sppo.partition_equal(S, N)
+    L = sppo.Layout(h, d, offsets)
+    x = {t: make_tensor(t, S, heads, d, seed=0, dtype=torch.bfloat16, device=dev) for t in ("q", "k", "v", "do")}
+    eng = engine.ChunkedAttention(ctx, L, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        eng.step(x["q"], x["k"], x["v"], x["do"], stream)
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    phase = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    for st in range(steps):
+        marks[st].record(stream)
+        eng.step(x["q"], x["k"], x["v"], x["do"], stream, mark=phase[st])
+    marks[steps].record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = marks[0].elapsed_time(marks[steps]) / steps
+    fwd_ms = sum(marks[i].elapsed_time(phase[i]) for i in range(steps)) / steps
+    bwd_ms = sum(phase[i].elapsed_time(marks[i + 1]) for i in range(steps)) / steps
+    fl = flops_of(offsets, h, d)
+    tf = fl / (ms * 1e-3) / 1e12
+    peaks = load_peaks()
+    ctx.close()
+    del eng, x
+    torch.cuda.empty_cache()
+    return {"workload": cfg["workload"], "value": round(tf, 2), "unit": "TFLOP/s", "ms_per_step": round(ms, 1),
+            "steps": steps, "warmup": warmup, "fwd_tflops": round(flops_of(offsets, h, d, "fwd") / (fwd_ms * 1e-3) / 1e12, 2),
+            "bwd_tflops": round(flops_of(offsets, h, d, "bwd") / (bwd_ms * 1e-3) / 1e12, 2),
+            "pct_bf16_peak": {"burst": round(100 * tf / peaks["burst"], 1),
+                              "sustained": round(100 * tf / peaks["sustained"], 1), "source": peaks["source"]},
+            "target": ">= 60 % of dense bf16 peak at 1M tokens on 1 GPU (BASELINE.json north_star)",
+            "clocks": clocks}
 
 
 # ------------------------------------------------------------------ context parallelism (SURVEY §8(f)2)
@@ -886,11 +974,40 @@ def main():
                     help="attention: the chunked attention hot path (headline); layer: full GPT layer per chunk")
     ap.add_argument("--parallel", default="heads", choices=["heads", "cp"],
                     help="multi-GPU split: heads (no collective in the step) or context-parallel ring")
+    ap.add_argument("--heads", type=int, default=0, help="override the config's head count (tests)")
+    ap.add_argument("--seq-len", type=int, default=0, help="override the config's S (tests)")
+    ap.add_argument("--chunks", type=int, default=0, help="override the config's N (tests)")
+    ap.add_argument("--o-digest", action="store_true",
+                    help="add sha256 of the (gathered) forward output O to the line (sharded == unsharded check)")
+    ap.add_argument("--no-c3", action="store_true",
+                    help="skip the bounded C3 (1M tokens, the north-star target) sub-measurement of the C2 line")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: warmup < 3 violates the timing rules", file=sys.stderr)
+    os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator / NVLS lines in the log (rank count evidence)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # plain `python bench.py --gpus N`: launch the N ranks ourselves (one process per GPU)
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    ws_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws_env != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}; launch with torchrun --nproc-per-node "
+              f"{args.gpus} or without torchrun", file=sys.stderr)
+        sys.exit(2)
     ws, rank, local = dist_setup()
-    cfg = CONFIGS[args.config]
+    numa = bind_numa(local) if args.impl == "ours" else None
+    cfg = dict(CONFIGS[args.config])
+    if args.heads or args.seq_len or args.chunks:  # test-size overrides: the line names the changed workload
+        cfg.update({k: v for k, v in (("heads", args.heads), ("S", args.seq_len), ("N", args.chunks)) if v})
+        cfg["workload"] = (f"{args.config} override (tests): {cfg['heads']} heads, d={cfg['d']}, S={cfg['S']}, "
+                           f"N={cfg['N']}, {cfg['dtype']}")
+    args.numa = numa
     if args.impl == "reference":
         line = run_reference(args, cfg, ws, rank)
     elif args.workload == "layer":

@@ -30,7 +30,7 @@
  * FP32 reference path, d <= 128).
  *
  * Ownership: the caller owns every device and host tensor passed in.  The
- * library owns only the ctx (copy streams, events, TMA descriptor cache,
+ * library owns only the ctx (copy streams, events, TMA descriptor ring,
  * window-coverage state) and host buffers returned by sppo_host_alloc.
  * No call frees caller memory.
  *
@@ -42,7 +42,11 @@
  *
  * Streams/events are passed as void* holding a cudaStream_t / cudaEvent_t
  * (NULL stream = legacy default stream).  No call synchronises the device
- * unless its name says so.
+ * unless its name says so.  (sppo_attn_fwd / sppo_attn_bwd may wait on the
+ * host for the kernel launched 128 compute calls earlier on the same ctx:
+ * each launch owns one block of a ring of TMA-descriptor tables, uploaded on
+ * the launch stream itself, and a block is reused only after its kernel
+ * completed.)
  */
 #ifndef SPPO_H_
 #define SPPO_H_
@@ -169,9 +173,17 @@ sppo_status sppo_finalize(sppo_ctx ctx, const float* src, void* dst, size_t n, i
 
 /* ---- two-level activation management: pinned host arena + copies ------- */
 
-/* Pinned (page-locked) host memory (P:472 [§7]: "page-locked memory").    */
+/* Pinned (page-locked) host memory, NUMA-local to the ctx's GPU (P:472 [§7]:
+ * "bind the NUMA node ... page-locked memory"): the GPU's node is read from
+ * sysfs at sppo_ctx_create; the pages are bound to it (mbind, preferred) before
+ * first touch and page-locked with cudaHostRegister.  When the node is unknown
+ * or the placement is refused, a portable cudaHostAlloc is used instead.
+ * Returns SPPO_E_OOM if neither succeeds.  Free with sppo_host_free (same ctx);
+ * sppo_ctx_destroy frees what is left. */
 sppo_status sppo_host_alloc(sppo_ctx ctx, size_t bytes, void** host);
 sppo_status sppo_host_free(sppo_ctx ctx, void* host);
+/* NUMA node of the ctx's GPU as seen by sppo_host_alloc (-1 = unknown). */
+sppo_status sppo_ctx_numa_node(sppo_ctx ctx, int32_t* node);
 
 /*
  * sppo_kv_offload — D2H copy of chunk `chunk`'s buffer prefix to host, on the

@@ -136,6 +136,11 @@ cudaError_t launch_col_reduce(int parts, const void* const* dy, const void* x, c
                               int64_t rows, int cols, float* sum_acc, float* prod_acc, int num_sms,
                               cudaStream_t s);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, current device).
+cudaError_t ensure_smem_attr(const void* fn, int bytes);
+// SM count of the current device.
+int num_sms();
+
 // error text for the ABI (thread-local; defined in sppo_api.cu)
 int api_fail(int status, const char* fmt, ...);
 

@@ -685,12 +685,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 cudaError_t launch_bwd_sm100(const Sm100Bwd& a, cudaStream_t s) {
   if (a.p.d != HD) return cudaErrorNotSupported;
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
+  cudaError_t e = ensure_smem_attr((const void*)bwd_kernel, kSmemBytes);
+  if (e != cudaSuccess) return e;
   dim3 grid(2 * a.pair_base[a.n], a.p.heads);
   bwd_kernel<<<grid, kThreads, kSmemBytes, s>>>(a);
   return cudaGetLastError();

@@ -438,12 +438,8 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
 
 cudaError_t launch_fwd_sm100(const Sm100Fwd& a, cudaStream_t s) {
   if (a.p.d != HD) return cudaErrorNotSupported;
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
+  cudaError_t e = ensure_smem_attr((const void*)fwd_kernel, kSmemBytes);
+  if (e != cudaSuccess) return e;
   dim3 grid((a.p.q_len + 2 * BM - 1) / (2 * BM), a.p.heads);
   fwd_kernel<<<grid, kThreads, kSmemBytes, s>>>(a);
   return cudaGetLastError();

@@ -467,12 +467,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 cudaError_t launch_pair(const CUtensorMap* ta, const CUtensorMap* tb, const GemmParams& p, int num_sms,
                         cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = ensure_smem_attr((const void*)gemm2_kernel, kPairSmem);
+  if (e != cudaSuccess) return e;
   const int tiles = ((p.M + 255) / 256) * (p.N / 256);
   const int clusters = tiles < num_sms / 2 ? tiles : num_sms / 2;
   gemm2_kernel<<<2 * clusters, kThreads, kPairSmem, s>>>(ta[0], ta[1], ta[2], *tb, p);
@@ -483,12 +479,8 @@ template <int BN>
 cudaError_t launch_bn(const CUtensorMap* ta, const CUtensorMap* tb, const GemmParams& p, int num_sms,
                       cudaStream_t s) {
   using C = Cfg<BN>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = ensure_smem_attr((const void*)gemm_kernel<BN>, C::kSmem);
+  if (e != cudaSuccess) return e;
   const int tiles = ((p.M + BM - 1) / BM) * (p.N / BN);
   const int grid = tiles < num_sms ? tiles : num_sms;
   gemm_kernel<BN><<<grid, kThreads, C::kSmem, s>>>(ta[0], ta[1], ta[2], *tb, p);

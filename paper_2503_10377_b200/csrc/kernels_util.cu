@@ -5,6 +5,10 @@
 // Coalesced 16-byte vector accesses; grid sized in multiples of the SM count.
 #include <cuda_bf16.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "internal.h"
 
 namespace sppo {
@@ -78,18 +82,28 @@ __global__ void cast_f32_f32_kernel(const float4* __restrict__ src, float4* __re
     dst[i] = src[i];
 }
 
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
+}  // namespace
+
+// Attributes are per device: remember (kernel, device) pairs, not a process-wide flag.
+cudaError_t ensure_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({fn, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({fn, dev});
+  return e;
 }
 
-}  // namespace
+int num_sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
 
 cudaError_t launch_bwd_preprocess(const BwdParams& p, bool bf16, cudaStream_t s) {
   const long long warps = (long long)p.q_len * p.heads;

@@ -9,9 +9,12 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include <mutex>
 #include <unordered_map>
-#include <unordered_set>
 #include <vector>
 
 #include "../../include/sppo.h"
@@ -80,7 +83,14 @@ struct DescKeyHash {
   }
 };
 
-constexpr int kDescSlots = 4096;
+// Descriptors of one launch form a block in a ring of device blocks; the block
+// is filled in pinned staging and uploaded with ONE cudaMemcpyAsync on the
+// launch stream right before the kernel, so a kernel only ever reads a table
+// written earlier on its own stream (no cross-stream ordering needed).  A block
+// is reused only after the event recorded behind its kernel has completed.
+constexpr int kDescBlockSlots = 8 + 2 * kMaxWindow;
+constexpr int kDescBlocks = 128;
+constexpr size_t kEncCacheMax = 1 << 16;
 
 struct Coverage {
   int32_t chunk;
@@ -93,15 +103,19 @@ struct sppo_ctx_s {
   int device = 0;
   cudaStream_t d2h = nullptr, h2d = nullptr;
   cudaEvent_t ev_prod = nullptr, ev_cons = nullptr, ev_copy = nullptr;
-  // TMA descriptor cache: device table + pinned staging (one slot each).
+  // TMA descriptors: host cache of encoded maps; per-launch blocks in a device
+  // ring (kDescBlocks x kDescBlockSlots) with pinned staging and a reuse event each.
   CUtensorMap* desc_dev = nullptr;
   CUtensorMap* desc_host = nullptr;
-  std::unordered_map<DescKey, int, DescKeyHash> desc_map;
-  std::vector<DescKey> desc_keys;
-  int desc_next = 0;
+  cudaEvent_t desc_ev[kDescBlocks] = {};
+  bool desc_ev_live[kDescBlocks] = {};
+  int desc_block_next = 0;
+  std::unordered_map<DescKey, CUtensorMap, DescKeyHash> enc_cache;
   // window coverage per (direction, q pointer)
   std::unordered_map<const void*, Coverage> cov_fwd, cov_bwd;
-  std::unordered_set<void*> host_allocs;
+  // host arena: ptr -> bytes (mmap + mbind + cudaHostRegister) or 0 (cudaHostAlloc fallback)
+  std::unordered_map<void*, size_t> host_allocs;
+  int numa_node = -1;  // NUMA node of the GPU (sysfs), -1 unknown
   std::mutex mu;
   // debug tracing (env SPPO_TRACE=<file>, SPPO_TRACE_CHUNK=<i>, SPPO_TRACE_KIND=fwd|bwd):
   // clock64 stamps of CTA (0,0) of one launch, dumped by sppo_ctx_sync
@@ -139,43 +153,69 @@ void trace_dump(sppo_ctx ctx) {
 
 namespace {
 
-// Returns the descriptor slot for a token-major [rows, heads, d] tensor of
-// bf16 (elem = 2) or fp32 (elem = 4), tiled as boxes of {128 B of d
-// (SWIZZLE_128B), 1 head, box_rows}.
-// A new descriptor is staged in pinned memory and copied to the device table
-// on `stream` (stream-ordered before the kernel that uses it).
-sppo_status get_desc(sppo_ctx ctx, const void* ptr, int64_t rows, int heads, int d, int box_rows,
-                     cudaStream_t stream, int* slot, int elem = 2) {
+// Encoded tensor map of a token-major [rows, heads, d] tensor of bf16 (elem = 2)
+// or fp32 (elem = 4), tiled as boxes of {128 B of d (SWIZZLE_128B), 1 head,
+// box_rows}; cached on the host by (ptr, shape).
+sppo_status encode_desc(sppo_ctx ctx, const void* ptr, int64_t rows, int heads, int d, int box_rows, int elem,
+                        CUtensorMap* out) {
   DescKey key{ptr, rows, heads, d, box_rows, elem};
-  auto it = ctx->desc_map.find(key);
-  if (it != ctx->desc_map.end()) {
-    *slot = it->second;
+  auto it = ctx->enc_cache.find(key);
+  if (it != ctx->enc_cache.end()) {
+    *out = it->second;
     return SPPO_OK;
   }
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(SPPO_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-  if (ctx->desc_next >= kDescSlots) {
-    // Table full: wait for all in-flight kernels, then recycle every slot.
-    SPPO_CUDA(cudaDeviceSynchronize(), "descriptor cache recycle");
-    ctx->desc_map.clear();
-    ctx->desc_next = 0;
-  }
-  const int s = ctx->desc_next++;
   cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)heads, (cuuint64_t)rows};
   cuuint64_t strides[2] = {(cuuint64_t)d * elem, (cuuint64_t)heads * d * elem};
   cuuint32_t box[3] = {(cuuint32_t)(128 / elem), 1, (cuuint32_t)box_rows};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(&ctx->desc_host[s], elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(out, elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SPPO_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  SPPO_CUDA(cudaMemcpyAsync(&ctx->desc_dev[s], &ctx->desc_host[s], sizeof(CUtensorMap), cudaMemcpyHostToDevice,
-                            stream),
-            "descriptor upload");
-  ctx->desc_map[key] = s;
-  *slot = s;
+  if (ctx->enc_cache.size() >= kEncCacheMax) ctx->enc_cache.clear();
+  ctx->enc_cache.emplace(key, *out);
   return SPPO_OK;
 }
+
+// The descriptor block of one launch.  Usage: open(), add() every map the
+// kernel reads (slot = index in the block), upload(stream) right before the
+// launch, close(stream) right after it.  Host-side failures before upload()
+// leave nothing enqueued.
+struct DescBlock {
+  sppo_ctx ctx;
+  int b = -1, n = 0;
+  sppo_status open(sppo_ctx c) {
+    ctx = c;
+    b = ctx->desc_block_next;
+    ctx->desc_block_next = (b + 1) % kDescBlocks;
+    n = 0;
+    // the staging and device block are free once the last kernel that used them finished
+    if (ctx->desc_ev_live[b]) SPPO_CUDA(cudaEventSynchronize(ctx->desc_ev[b]), "descriptor block reuse");
+    ctx->desc_ev_live[b] = false;
+    return SPPO_OK;
+  }
+  sppo_status add(const void* ptr, int64_t rows, int heads, int d, int box_rows, int* slot, int elem = 2) {
+    if (n >= kDescBlockSlots) return fail(SPPO_E_UNSUPPORTED, "too many descriptors in one launch");
+    sppo_status s = encode_desc(ctx, ptr, rows, heads, d, box_rows, elem, &ctx->desc_host[b * kDescBlockSlots + n]);
+    if (s) return s;
+    *slot = n++;
+    return SPPO_OK;
+  }
+  const void* table() const { return ctx->desc_dev + (size_t)b * kDescBlockSlots; }
+  sppo_status upload(cudaStream_t stream) {
+    SPPO_CUDA(cudaMemcpyAsync(ctx->desc_dev + (size_t)b * kDescBlockSlots, ctx->desc_host + (size_t)b * kDescBlockSlots,
+                              sizeof(CUtensorMap) * n, cudaMemcpyHostToDevice, stream),
+              "descriptor upload");
+    return SPPO_OK;
+  }
+  sppo_status close(cudaStream_t stream) {
+    SPPO_CUDA(cudaEventRecord(ctx->desc_ev[b], stream), "descriptor block event");
+    ctx->desc_ev_live[b] = true;
+    return SPPO_OK;
+  }
+};
 
 // ---------------------------------------------------------------- validation
 sppo_status check_layout(const sppo_layout* L, int32_t chunk) {
@@ -264,6 +304,45 @@ void fill_window(const sppo_layout* L, const sppo_kv_set* kv, KvWindow* w) {
 
 }  // namespace
 
+namespace {
+// NUMA node of a GPU from sysfs (/sys/bus/pci/devices/<bus id>/numa_node), -1 if unknown.
+int gpu_numa_node(int device) {
+  char bus[64] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) return -1;
+  unsigned dom = 0, b = 0, d = 0, f = 0;
+  if (sscanf(bus, "%x:%x:%x.%x", &dom, &b, &d, &f) != 4) return -1;
+  char path[128];
+  snprintf(path, sizeof path, "/sys/bus/pci/devices/%04x:%02x:%02x.%x/numa_node", dom & 0xffffu, b, d, f);
+  FILE* fp = fopen(path, "r");
+  if (!fp) return -1;
+  int node = -1;
+  if (fscanf(fp, "%d", &node) != 1) node = -1;
+  fclose(fp);
+  return node;
+}
+
+// Page-locked host memory placed on `node` (P:472 [§7]: "bind the NUMA node ...
+// page-locked memory"): anonymous mapping, mbind(MPOL_PREFERRED) before first
+// touch, then cudaHostRegister (which faults the pages in, on that node).
+void* numa_pinned_alloc(size_t bytes, int node) {
+  if (node < 0 || node >= 64) return nullptr;
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (p == MAP_FAILED) return nullptr;
+  unsigned long mask = 1ul << node;
+  const int kMpolPreferred = 1;
+  if (syscall(SYS_mbind, p, bytes, kMpolPreferred, &mask, (unsigned long)(8 * sizeof mask), 0u) != 0) {
+    munmap(p, bytes);
+    return nullptr;
+  }
+  if (cudaHostRegister(p, bytes, cudaHostRegisterPortable) != cudaSuccess) {
+    cudaGetLastError();
+    munmap(p, bytes);
+    return nullptr;
+  }
+  return p;
+}
+}  // namespace
+
 int sppo::api_fail(int status, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
@@ -294,11 +373,18 @@ sppo_status sppo_ctx_create(int device, sppo_ctx* out) {
       (e = cudaEventCreateWithFlags(&c->ev_prod, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&c->ev_cons, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming)) != cudaSuccess ||
-      (e = cudaMalloc(&c->desc_dev, sizeof(CUtensorMap) * kDescSlots)) != cudaSuccess ||
-      (e = cudaHostAlloc(&c->desc_host, sizeof(CUtensorMap) * kDescSlots, cudaHostAllocDefault)) != cudaSuccess) {
+      (e = cudaMalloc(&c->desc_dev, sizeof(CUtensorMap) * kDescBlockSlots * kDescBlocks)) != cudaSuccess ||
+      (e = cudaHostAlloc(&c->desc_host, sizeof(CUtensorMap) * kDescBlockSlots * kDescBlocks, cudaHostAllocDefault)) !=
+          cudaSuccess) {
     sppo_ctx_destroy(c);
     return cuda_fail(e, "sppo_ctx_create");
   }
+  for (int b = 0; b < kDescBlocks; ++b)
+    if ((e = cudaEventCreateWithFlags(&c->desc_ev[b], cudaEventDisableTiming)) != cudaSuccess) {
+    sppo_ctx_destroy(c);
+    return cuda_fail(e, "sppo_ctx_create");
+  }
+  c->numa_node = gpu_numa_node(device);
   if (getenv("SPPO_TRACE")) {
     const char* ch = getenv("SPPO_TRACE_CHUNK");
     const char* kind = getenv("SPPO_TRACE_KIND");
@@ -316,12 +402,21 @@ sppo_status sppo_ctx_destroy(sppo_ctx c) {
   if (!c) return fail(SPPO_E_ARG, "ctx is NULL");
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  for (void* h : c->host_allocs) cudaFreeHost(h);
+  for (auto& kv : c->host_allocs) {
+    if (kv.second) {
+      cudaHostUnregister(kv.first);
+      munmap(kv.first, kv.second);
+    } else {
+      cudaFreeHost(kv.first);
+    }
+  }
   if (c->d2h) cudaStreamDestroy(c->d2h);
   if (c->h2d) cudaStreamDestroy(c->h2d);
   if (c->ev_prod) cudaEventDestroy(c->ev_prod);
   if (c->ev_cons) cudaEventDestroy(c->ev_cons);
   if (c->ev_copy) cudaEventDestroy(c->ev_copy);
+  for (int b = 0; b < kDescBlocks; ++b)
+    if (c->desc_ev[b]) cudaEventDestroy(c->desc_ev[b]);
   if (c->desc_dev) cudaFree(c->desc_dev);
   if (c->desc_host) cudaFreeHost(c->desc_host);
   if (c->trace) cudaFree(c->trace);
@@ -381,15 +476,16 @@ sppo_status sppo_attn_fwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
   }
   cudaError_t e;
   if (L->dtype == SPPO_FP32) {
-    static KvWindow w;  // large; guarded by ctx->mu
+    KvWindow w;  // per call: no state shared between contexts or threads
     fill_window(L, kv, &w);
     e = launch_fwd_simt_f32(p, w, strm);
   } else {
-    static Sm100Fwd a;
+    Sm100Fwd a{};
     a.p = p;
     a.n = kv->n;
-    a.desc_table = ctx->desc_dev;
-    if ((s = get_desc(ctx, q, p.q_len, p.heads, p.d, 128, strm, &a.q_slot))) return s;
+    DescBlock db;
+    if ((s = db.open(ctx))) return s;
+    if ((s = db.add(q, p.q_len, p.heads, p.d, 128, &a.q_slot))) return s;
     // kernel contract: the diagonal chunk (id == chunk), if present, is visited last
     std::vector<int> order;
     for (int c = 0; c < kv->n; ++c)
@@ -403,12 +499,15 @@ sppo_status sppo_attn_fwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
       a.start[oc] = (int32_t)L->offsets[j];
       a.len[oc] = (int32_t)len;
       int sk, sv;
-      if ((s = get_desc(ctx, kv->k[c], len, p.heads, p.d, 128, strm, &sk))) return s;
-      if ((s = get_desc(ctx, kv->v[c], len, p.heads, p.d, 128, strm, &sv))) return s;
+      if ((s = db.add(kv->k[c], len, p.heads, p.d, 128, &sk))) return s;
+      if ((s = db.add(kv->v[c], len, p.heads, p.d, 128, &sv))) return s;
       a.slots.k[oc] = (uint16_t)sk;
       a.slots.v[oc] = (uint16_t)sv;
     }
+    a.desc_table = db.table();
+    if ((s = db.upload(strm))) return s;
     e = launch_fwd_sm100(a, strm);
+    if (e == cudaSuccess && (s = db.close(strm))) return s;
   }
   if (e == cudaErrorNotSupported) return fail(SPPO_E_UNSUPPORTED, "this request is not implemented by the sm_100a kernels");
   if (e != cudaSuccess) return cuda_fail(e, "sppo_attn_fwd launch");
@@ -468,43 +567,50 @@ sppo_status sppo_attn_bwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
   p.trace = trace_for(ctx, chunk, true);
   const bool bf16 = L->dtype == SPPO_BF16;
   cudaError_t e = cudaSuccess;
-  if (first) e = launch_bwd_preprocess(p, bf16, strm);  // Delta_i, dq_acc = 0  (a5)
-  if (e != cudaSuccess) return cuda_fail(e, "bwd preprocess");
-  static KvWindow w;
-  static KvGradWindow g;
+  // host-side preparation first (nothing is enqueued if it fails), then
+  // Delta_i / dq_acc = 0 on FIRST (a5), then the main kernel
+  auto preprocess = [&]() { return first ? launch_bwd_preprocess(p, bf16, strm) : cudaSuccess; };
+  KvWindow w;  // per call: no state shared between contexts or threads
   fill_window(L, kv, &w);
-  for (int c = 0; c < kv->n; ++c) {
-    g.dk[c] = a->dk_acc[c];
-    g.dv[c] = a->dv_acc[c];
-  }
   if (!bf16) {
+    KvGradWindow g;
+    for (int c = 0; c < kv->n; ++c) {
+      g.dk[c] = a->dk_acc[c];
+      g.dv[c] = a->dv_acc[c];
+    }
+    if ((e = preprocess()) != cudaSuccess) return cuda_fail(e, "bwd preprocess");
     e = launch_bwd_simt_f32(p, w, g, strm);
   } else {
-    static Sm100Bwd sa;
+    Sm100Bwd sa{};
     sa.p = p;
     sa.n = kv->n;
-    sa.desc_table = ctx->desc_dev;
-    if ((s = get_desc(ctx, q, p.q_len, p.heads, p.d, 128, strm, &sa.q_slot))) return s;
-    if ((s = get_desc(ctx, a->dout, p.q_len, p.heads, p.d, 128, strm, &sa.do_slot))) return s;
-    if ((s = get_desc(ctx, q, p.q_len, p.heads, p.d, 64, strm, &sa.q64_slot))) return s;
-    if ((s = get_desc(ctx, a->dout, p.q_len, p.heads, p.d, 64, strm, &sa.do64_slot))) return s;
-    if ((s = get_desc(ctx, a->dq_acc, p.q_len, p.heads, p.d, 128, strm, &sa.dq_slot, 4))) return s;
+    DescBlock db;
+    if ((s = db.open(ctx))) return s;
+    if ((s = db.add(q, p.q_len, p.heads, p.d, 128, &sa.q_slot))) return s;
+    if ((s = db.add(a->dout, p.q_len, p.heads, p.d, 128, &sa.do_slot))) return s;
+    if ((s = db.add(q, p.q_len, p.heads, p.d, 64, &sa.q64_slot))) return s;
+    if ((s = db.add(a->dout, p.q_len, p.heads, p.d, 64, &sa.do64_slot))) return s;
+    if ((s = db.add(a->dq_acc, p.q_len, p.heads, p.d, 128, &sa.dq_slot, 4))) return s;
     int pairs = 0;
     for (int c = 0; c < kv->n; ++c) {
       int sk, sv;
-      if ((s = get_desc(ctx, kv->k[c], w.len[c], p.heads, p.d, 128, strm, &sk))) return s;
-      if ((s = get_desc(ctx, kv->v[c], w.len[c], p.heads, p.d, 128, strm, &sv))) return s;
+      if ((s = db.add(kv->k[c], w.len[c], p.heads, p.d, 128, &sk))) return s;
+      if ((s = db.add(kv->v[c], w.len[c], p.heads, p.d, 128, &sv))) return s;
       sa.slots.k[c] = (uint16_t)sk;
       sa.slots.v[c] = (uint16_t)sv;
       sa.start[c] = w.start[c];
       sa.len[c] = w.len[c];
       sa.pair_base[c] = pairs;
       pairs += (w.len[c] + 255) / 256;
-      sa.dk[c] = g.dk[c];
-      sa.dv[c] = g.dv[c];
+      sa.dk[c] = a->dk_acc[c];
+      sa.dv[c] = a->dv_acc[c];
     }
     sa.pair_base[kv->n] = pairs;
+    sa.desc_table = db.table();
+    if ((e = preprocess()) != cudaSuccess) return cuda_fail(e, "bwd preprocess");
+    if ((s = db.upload(strm))) return s;
     e = launch_bwd_sm100(sa, strm);
+    if (e == cudaSuccess && (s = db.close(strm))) return s;
   }
   if (e == cudaErrorNotSupported) return fail(SPPO_E_UNSUPPORTED, "this request is not implemented by the sm_100a kernels");
   if (e != cudaSuccess) return cuda_fail(e, "sppo_attn_bwd launch");
@@ -522,11 +628,18 @@ sppo_status sppo_host_alloc(sppo_ctx ctx, size_t bytes, void** host) {
   *host = nullptr;
   if (!bytes) return fail(SPPO_E_ARG, "bytes = 0");
   SPPO_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
-  void* p = nullptr;
-  cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
-  if (e != cudaSuccess) return fail(SPPO_E_OOM, "cudaHostAlloc(%zu): %s", bytes, cudaGetErrorString(e));
+  // NUMA-local to the GPU when its node is known; otherwise (or if the node is
+  // out of memory / mbind is refused) a plain portable cudaHostAlloc
+  size_t mapped = 0;
+  void* p = numa_pinned_alloc(bytes, ctx->numa_node);
+  if (p) {
+    mapped = bytes;
+  } else {
+    cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) return fail(SPPO_E_OOM, "cudaHostAlloc(%zu): %s", bytes, cudaGetErrorString(e));
+  }
   std::lock_guard<std::mutex> lock(ctx->mu);
-  ctx->host_allocs.insert(p);
+  ctx->host_allocs[p] = mapped;
   *host = p;
   return SPPO_OK;
 }
@@ -536,8 +649,20 @@ sppo_status sppo_host_free(sppo_ctx ctx, void* host) {
   std::lock_guard<std::mutex> lock(ctx->mu);
   auto it = ctx->host_allocs.find(host);
   if (it == ctx->host_allocs.end()) return fail(SPPO_E_ARG, "pointer not from sppo_host_alloc");
+  const size_t mapped = it->second;
   ctx->host_allocs.erase(it);
-  SPPO_CUDA(cudaFreeHost(host), "cudaFreeHost");
+  if (mapped) {
+    SPPO_CUDA(cudaHostUnregister(host), "cudaHostUnregister");
+    if (munmap(host, mapped) != 0) return fail(SPPO_E_ARG, "munmap failed");
+  } else {
+    SPPO_CUDA(cudaFreeHost(host), "cudaFreeHost");
+  }
+  return SPPO_OK;
+}
+
+sppo_status sppo_ctx_numa_node(sppo_ctx ctx, int32_t* node) {
+  if (!ctx || !node) return fail(SPPO_E_ARG, "ctx/node is NULL");
+  *node = ctx->numa_node;
   return SPPO_OK;
 }
 

@@ -25,9 +25,28 @@ sized for the longest chunk and reused.
 
 from __future__ import annotations
 
+import functools
+import inspect
+
 import torch
 
 from . import sppo
+
+
+def _on_step_stream(fn):
+    """Runs a step method with torch's current stream set to its ``stream``
+    argument, so the torch-side work inside it (accumulator zeroing, poison
+    fills, allocations) is ordered with the ABI calls enqueued on that stream."""
+    sig = inspect.signature(fn)
+
+    @functools.wraps(fn)
+    def run(self, *args, **kwargs):
+        b = sig.bind(self, *args, **kwargs)
+        strm = b.arguments.get("stream") or torch.cuda.current_stream()
+        b.arguments["stream"] = strm
+        with torch.cuda.stream(strm):
+            return fn(*b.args, **b.kwargs)
+    return run
 
 DTYPES = {sppo.SPPO_BF16: torch.bfloat16, sppo.SPPO_FP32: torch.float32}
 
@@ -180,6 +199,7 @@ class ChunkedAttention:
             end.record(strm)
 
     # one step, all activations resident ---------------------------------------
+    @_on_step_stream
     def step(self, q, k, v, do, stream=None, mark=None):
         """Full forward + backward over all chunks (resident policy).  ``mark``
         (a torch.cuda.Event) is recorded between the forward and backward phases."""
@@ -223,6 +243,7 @@ class ChunkedAttention:
             self.ctx.host_free(ptr)
         self._host.clear()
 
+    @_on_step_stream
     def step_offload(self, q, k, v, do, alpha, stream=None, depth: int = 2, poison: bool = False, mark=None):
         """Forward + backward where Q_i, O_i and LSE_i leave the GPU after fwd(i)
         (alpha_i-prefix of each token-major buffer, LSE whole when alpha_i > 0)
@@ -290,6 +311,7 @@ class ChunkedAttention:
         return moved
 
     # one step with KV streaming (hot prefix resident, cold chunks on host) -----
+    @_on_step_stream
     def step_kv_stream(self, q, k, v, do, hot: int, window: int, stream=None, poison: bool = False):
         """Forward + backward with the KV residency policy of SURVEY §8(c):
         K_j, V_j of the hot prefix j < ``hot`` stay on the GPU (the most-accessed
@@ -415,6 +437,7 @@ class ChunkedAttention:
                 self._last_off_ev = poison_ev
         return stats
 
+    @_on_step_stream
     def step_kv_stream_grouped(self, q, k, v, do, hot: int, window: int, group: int = 2, stream=None,
                                poison: bool = False):
         """KV streaming (step_kv_stream's policy, L10) with the cold windows shared
@@ -561,6 +584,7 @@ class ChunkedAttention:
         return stats
 
     # end-to-end step through host buffers --------------------------------------
+    @_on_step_stream
     def step_host_io(self, host_in, host_out, dev_in, stream=None):
         """One step whose inputs start in pinned host memory and whose results end
         there: chunk-wise H2D of Q_i, K_i, V_i, dO_i (sppo_kv_prefetch, deferred
@@ -582,30 +606,43 @@ class ChunkedAttention:
             nb = t.numel() * t.element_size()
             off = L.offsets[i] * L.heads * L.head_dim * self.elem
             ev = torch.cuda.Event()
+            # ordered after the work already on `strm` (a previous step still reading the
+            # device inputs); nothing of this step is enqueued yet, so the copies of this
+            # step do not wait for each other's consumers
             self.ctx.kv_prefetch(i, host_in[name] + off, t, nb, consumer=strm, done=ev,
-                                 flags=sppo.SPPO_COPY_NO_ORDER | sppo.SPPO_COPY_DEFER_WAIT)
+                                 flags=sppo.SPPO_COPY_DEFER_WAIT)
             h2d += nb
             ready[i][j] = ev
         self.dk_acc.zero_()
         self.dv_acc.zero_()
+        # the device result rows of chunk i are rewritten only after the previous
+        # call's D2H of those rows has completed (WAR on o / dq / dk / dv)
+        prev = getattr(self, "_io_prev", {})
+        self._io_prev = cur = {}
         last = None
         for i in range(N):
             for ev in ready[i][:3]:
                 strm.wait_event(ev)
+            if ("o", i) in prev:
+                strm.wait_event(prev[("o", i)])
             self.forward_chunk(i, dev_in["q"], dev_in["k"], dev_in["v"], strm)
             t = self.rows(self.o, i)
             nb = t.numel() * t.element_size()
             off = L.offsets[i] * L.heads * L.head_dim * self.elem
             last = torch.cuda.Event()
             d2h += self.ctx.kv_offload(i, t, host_out["o"] + off, nb, 1.0, producer=strm, done=last)
+            cur[("o", i)] = last
         for i in range(N - 1, -1, -1):
             strm.wait_event(ready[i][3])
+            if ("g", i) in prev:
+                strm.wait_event(prev[("g", i)])
             self.backward_chunk(i, dev_in["q"], dev_in["k"], dev_in["v"], dev_in["do"], strm)
             for name, t in (("dq", self.rows(self.dq, i)), ("dk", self.rows(self.dk, i)), ("dv", self.rows(self.dv, i))):
                 nb = t.numel() * t.element_size()
                 off = L.offsets[i] * L.heads * L.head_dim * self.elem
                 last = torch.cuda.Event()
                 d2h += self.ctx.kv_offload(i, t, host_out[name] + off, nb, 1.0, producer=strm, done=last)
+            cur[("g", i)] = last  # the copies run in order on the D2H stream: the last covers all three
         return h2d, d2h, last
 
     def lse_heads_major(self):

@@ -388,35 +388,47 @@ class ChunkedLayer:
         row = H * 2
         ready_x, ready_dz = [], [None] * self.N
         h2d = d2h = 0
+        # copies are ordered after the work already on `strm` (a previous step still
+        # reading x / dz); nothing of this step is enqueued yet, so they do not wait
+        # on each other's consumers
         for i in range(self.N):  # issue order = consumption order on the H2D stream
             ev = torch.cuda.Event()
             nb = (c[i + 1] - c[i]) * row
             self.ctx.kv_prefetch(i, host_x + c[i] * row, self.rows(x, i), nb, consumer=strm, done=ev,
-                                 flags=sppo.SPPO_COPY_NO_ORDER | sppo.SPPO_COPY_DEFER_WAIT)
+                                 flags=sppo.SPPO_COPY_DEFER_WAIT)
             ready_x.append(ev)
             h2d += nb
         for i in range(self.N - 1, -1, -1):
             ev = torch.cuda.Event()
             nb = (c[i + 1] - c[i]) * row
             self.ctx.kv_prefetch(i, host_dz + c[i] * row, self.rows(dz, i), nb, consumer=strm, done=ev,
-                                 flags=sppo.SPPO_COPY_NO_ORDER | sppo.SPPO_COPY_DEFER_WAIT)
+                                 flags=sppo.SPPO_COPY_DEFER_WAIT)
             ready_dz[i] = ev
             h2d += nb
         self._zero()
+        # z_i / dx_i device rows are rewritten only after the previous call's D2H of them (WAR)
+        prev = getattr(self, "_io_prev", {})
+        self._io_prev = cur = {}
         last = None
         for i in range(self.N):
             strm.wait_event(ready_x[i])
+            if ("z", i) in prev:
+                strm.wait_event(prev[("z", i)])
             self.forward_chunk(i, x, strm)
             nb = (c[i + 1] - c[i]) * row
             last = torch.cuda.Event()
             d2h += self.ctx.kv_offload(i, self.rows(self.z, i), host_z + c[i] * row, nb, 1.0, producer=strm, done=last)
+            cur[("z", i)] = last
         for i in range(self.N - 1, -1, -1):
             strm.wait_event(ready_dz[i])
+            if ("dx", i) in prev:
+                strm.wait_event(prev[("dx", i)])
             self.backward_chunk(i, x, dz, strm)
             nb = (c[i + 1] - c[i]) * row
             last = torch.cuda.Event()
             d2h += self.ctx.kv_offload(i, self.rows(self.dx, i), host_dx + c[i] * row, nb, 1.0, producer=strm,
                                        done=last)
+            cur[("dx", i)] = last
         return h2d, d2h, last
 
     # ------------------------------------------------------------------ Type-1 offload with alpha

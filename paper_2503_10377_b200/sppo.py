@@ -29,7 +29,7 @@ EXPORTS = ("sppo_ctx_create", "sppo_ctx_destroy", "sppo_ctx_sync", "sppo_last_er
            "sppo_attn_fwd", "sppo_attn_bwd", "sppo_host_alloc", "sppo_host_free", "sppo_kv_offload",
            "sppo_kv_prefetch", "sppo_partition_equal", "sppo_partition_balanced", "sppo_partition_balanced_lin", "sppo_causal_pairs",
            "sppo_offload_alpha",
-           "sppo_finalize", "sppo_ctx_streams")
+           "sppo_finalize", "sppo_ctx_streams", "sppo_ctx_numa_node")
 # every symbol include/sppo_layer.h declares (per-chunk transformer layer)
 LAYER_EXPORTS = ("sppo_gemm", "sppo_layernorm_fwd", "sppo_layernorm_bwd", "sppo_col_reduce")
 # every symbol include/sppo_pipeline.h declares (subsequence pipeline plan)
@@ -98,6 +98,7 @@ def _load():
                                 C.POINTER(C.c_double)], i32),
         "sppo_finalize": ([vp, vp, vp, sz, i32, vp], i32),
         "sppo_ctx_streams": ([vp, C.POINTER(vp), C.POINTER(vp)], i32),
+        "sppo_ctx_numa_node": ([vp, C.POINTER(i32)], i32),
         "sppo_gemm": ([vp, C.POINTER(_GemmArgs), vp], i32),
         "sppo_msp_phases": ([i32, i32, i32, C.POINTER(C.c_int8), C.POINTER(i32), C.POINTER(i32)], i32),
         "sppo_pipeline_bubble": ([i32, i32, C.POINTER(C.c_double)], i32),
@@ -264,6 +265,12 @@ class Context:
         a, b = C.c_void_p(), C.c_void_p()
         _check(_lib.sppo_ctx_streams(self.h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def numa_node(self) -> int:
+        """NUMA node of this ctx's GPU used by host_alloc (sppo_ctx_numa_node; -1 unknown)."""
+        n = C.c_int32()
+        _check(_lib.sppo_ctx_numa_node(self.h, C.byref(n)))
+        return n.value
 
     # -------------------------------------------------------------- attention
     def attn_fwd(self, layout: Layout, chunk: int, q, kv_ids, ks, vs, flags=SPPO_FIRST | SPPO_LAST, state=None,

@@ -39,3 +39,13 @@ def test_flop_accounting_matches_oracle():
 def test_clock_reject_set():
     assert bench.CLOCK_REJECT == {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
     assert "sw_power_cap" not in bench.CLOCK_REJECT  # kept and noted, per the timing rules
+
+
+def test_bench_refuses_world_size_mismatch():
+    """--gpus N must match the launcher's WORLD_SIZE (a mis-launched multi-GPU
+    run would otherwise report the wrong n_gpus)."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--config", "C1"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=300, env={**os.environ, "WORLD_SIZE": "1"})
+    assert r.returncode == 2 and "WORLD_SIZE=1" in r.stderr

@@ -57,3 +57,19 @@ def test_bench_device_budget_picks_hot_prefix_c1():
               "--no-offload", "--device-budget", "0.0027", "--kv-window", "1"])
     b = d["kv_stream"]["budget"]
     assert 0 <= b["hot_prefix_chosen"] < 4 and b["resident_bytes"] <= 0.0027e9 < b["all_resident_bytes"]
+
+
+def test_bench_plain_gpus2_self_launches_head_sharded():
+    """`python bench.py --gpus 2` without torchrun launches the two ranks itself
+    (here sharing the one GPU over gloo); the line reports n_gpus = 2 and the
+    gathered O equals the unsharded run bit for bit (inputs are generated per
+    global head and the forward is deterministic, reading L12)."""
+    small = ["--config", "C2", "--heads", "4", "--seq-len", "4096", "--chunks", "4", "--steps", "3", "--warmup",
+             "3", "--no-cpu", "--no-e2e", "--no-offload", "--o-digest"]
+    one = _run([sys.executable, "bench.py", "--gpus", "1"] + small)
+    two = _run([sys.executable, "bench.py", "--gpus", "2"] + small,
+               env={"SPPO_BENCH_DEVICE": "0", "SPPO_DIST_BACKEND": "gloo"})
+    assert one["n_gpus"] == 1 and two["n_gpus"] == 2
+    assert two["config"]["heads_per_gpu"] == 2 and one["config"]["heads_per_gpu"] == 4
+    assert two["gather"] is not None and two["gather"]["bytes"] == 4096 * 4 * 128 * 2
+    assert one["o_sha256"] == two["o_sha256"]
