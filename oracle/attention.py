@@ -321,10 +321,15 @@ def sampled_rows(q, k, v, rows, do=None, heads=None, scale=None):
 
 
 def sampled_key_grads(q, k, v, do, keys, heads=None, scale=None, row_block=256):
-    """dK_t, dV_t for selected keys t, from the definition: they need every row
-    p >= t, each row's LSE_p and Delta_p computed from its own full prefix.
-    Cost O((S - min(keys)) * S * d) per head, so pick keys near the end.
-    Returns dict(dk [K,H,d], dv [K,H,d]).
+    """dK_t, dV_t for selected keys t, from the definition:
+        dV_t = sum_{p >= t} P_pt dO_p,   dK_t = tau sum_{p >= t} dS_pt q_p,
+        dS_pt = P_pt (<dO_p, v_t> - Delta_p),  Delta_p = <dO_p, O_p>,
+    where every row p >= min(keys) gets its exact P row, LSE_p and O_p from its
+    own full causal prefix (keys 0..p).  Rows are taken in blocks of
+    ``row_block``; a block [r0, r1) only needs keys < r1 (causality), and only
+    its diagonal square needs the t > p mask.
+    Cost O((S - min(keys)) * S * d) per head, so pick keys near the end unless
+    the time is affordable.  Returns dict(dk [K,H,d], dv [K,H,d]).
     """
     keys = np.asarray([int(t) for t in keys])
     S, _, d = q.shape
@@ -338,20 +343,23 @@ def sampled_key_grads(q, k, v, do, keys, heads=None, scale=None, row_block=256):
         kh = np.asarray(k[:, hh, :], dtype=np.float64)
         vh = np.asarray(v[:, hh, :], dtype=np.float64)
         doh = np.asarray(do[:, hh, :], dtype=np.float64)
+        vk = vh[keys]
         for r0 in range(t0, S, row_block):
             r1 = min(S, r0 + row_block)
-            kc = max(r1, int(keys.max()) + 1)                      # keys 0..kc (t > p masked)
-            s = tau * (qh[r0:r1] @ kh[:kc].T)
-            vis = np.arange(kc)[None, :] <= np.arange(r0, r1)[:, None]
-            s = np.where(vis, s, -np.inf)
+            s = tau * (qh[r0:r1] @ kh[:r1].T)                       # rows r0..r1-1, keys 0..r1-1
+            diag = s[:, r0:r1]
+            diag[np.triu_indices(r1 - r0, 1)] = -np.inf              # t > p masked
             m = s.max(axis=1, keepdims=True)
-            e = np.exp(s - m)
-            l = e.sum(axis=1, keepdims=True)
-            p = e / l                                               # exact P rows
-            o = p @ vh[:kc]
+            np.subtract(s, m, out=s)
+            np.exp(s, out=s)
+            l = s.sum(axis=1, keepdims=True)
+            np.divide(s, l, out=s)                                   # s now holds the exact P rows
+            o = s @ vh[:r1]
             delta = np.einsum("rd,rd->r", doh[r0:r1], o)
-            pk = p[:, keys]                                         # [rows, K]
-            dpk = doh[r0:r1] @ vh[keys].T                           # [rows, K]
+            pk = np.zeros((r1 - r0, len(keys)))
+            vis = keys < r1                                          # keys no row of the block sees: P = 0
+            pk[:, vis] = s[:, keys[vis]]
+            dpk = doh[r0:r1] @ vk.T                                  # [rows, K]
             dsk = pk * (dpk - delta[:, None])
             dv[:, n] += pk.T @ doh[r0:r1]
             dk[:, n] += tau * (dsk.T @ qh[r0:r1])

@@ -13,6 +13,7 @@
 #include <sys/syscall.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
@@ -83,14 +84,20 @@ struct DescKeyHash {
   }
 };
 
-// Descriptors of one launch form a block in a ring of device blocks; the block
-// is filled in pinned staging and uploaded with ONE cudaMemcpyAsync on the
-// launch stream right before the kernel, so a kernel only ever reads a table
-// written earlier on its own stream (no cross-stream ordering needed).  A block
-// is reused only after the event recorded behind its kernel has completed.
-constexpr int kDescBlockSlots = 8 + 2 * kMaxWindow;
-constexpr int kDescBlocks = 128;
-constexpr size_t kEncCacheMax = 1 << 16;
+// TMA descriptors live in ONE persistent device table of kDescSlots maps.  A
+// map (key: pointer + shape) is encoded on the host and uploaded once, the
+// first time a call needs it: one cudaMemcpyAsync of the call's new maps on
+// the launch stream, followed by an event.  Later calls that hit the slot from
+// another stream make their stream wait on that event until its completion has
+// been observed once, so a kernel never reads a table entry whose upload is
+// unordered with it.  In the steady state (same buffers every step)
+// no call uploads anything, so no descriptor copy ever queues behind the large
+// offload / prefetch copies on the copy engines.  When a call's new maps do not
+// fit, the table is recycled BEFORE any slot of that call is resolved, after
+// every stream that launched from the table has drained (host wait; rare).
+constexpr int kDescSlots = 16384;          // kernels take uint16_t slot indices
+constexpr int kDescCallMax = 8 + 2 * kMaxWindow;
+constexpr int kUploadEvents = 64;
 
 struct Coverage {
   int32_t chunk;
@@ -103,14 +110,24 @@ struct sppo_ctx_s {
   int device = 0;
   cudaStream_t d2h = nullptr, h2d = nullptr;
   cudaEvent_t ev_prod = nullptr, ev_cons = nullptr, ev_copy = nullptr;
-  // TMA descriptors: host cache of encoded maps; per-launch blocks in a device
-  // ring (kDescBlocks x kDescBlockSlots) with pinned staging and a reuse event each.
+  // TMA descriptors: persistent device table + pinned host mirror, key -> slot,
+  // per-slot upload record (event id, its generation, upload stream, observed done)
   CUtensorMap* desc_dev = nullptr;
   CUtensorMap* desc_host = nullptr;
-  cudaEvent_t desc_ev[kDescBlocks] = {};
-  bool desc_ev_live[kDescBlocks] = {};
-  int desc_block_next = 0;
-  std::unordered_map<DescKey, CUtensorMap, DescKeyHash> enc_cache;
+  std::unordered_map<DescKey, int, DescKeyHash> desc_slot;
+  struct SlotUpload {
+    int ev = -1;
+    uint32_t gen = 0;
+    cudaStream_t stream = nullptr;
+    bool done = true;
+  };
+  std::vector<SlotUpload> slot_up;
+  int desc_next = 0;
+  cudaEvent_t up_ev[kUploadEvents] = {};
+  uint32_t up_gen[kUploadEvents] = {};
+  bool up_live[kUploadEvents] = {};
+  int up_next = 0;
+  std::vector<cudaStream_t> desc_streams;  // streams that launched from the table since the last recycle
   // window coverage per (direction, q pointer)
   std::unordered_map<const void*, Coverage> cov_fwd, cov_bwd;
   // host arena: ptr -> bytes (mmap + mbind + cudaHostRegister) or 0 (cudaHostAlloc fallback)
@@ -155,64 +172,117 @@ namespace {
 
 // Encoded tensor map of a token-major [rows, heads, d] tensor of bf16 (elem = 2)
 // or fp32 (elem = 4), tiled as boxes of {128 B of d (SWIZZLE_128B), 1 head,
-// box_rows}; cached on the host by (ptr, shape).
-sppo_status encode_desc(sppo_ctx ctx, const void* ptr, int64_t rows, int heads, int d, int box_rows, int elem,
-                        CUtensorMap* out) {
-  DescKey key{ptr, rows, heads, d, box_rows, elem};
-  auto it = ctx->enc_cache.find(key);
-  if (it != ctx->enc_cache.end()) {
-    *out = it->second;
-    return SPPO_OK;
-  }
+// box_rows}.
+sppo_status encode_desc(const DescKey& key, CUtensorMap* out) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(SPPO_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)heads, (cuuint64_t)rows};
-  cuuint64_t strides[2] = {(cuuint64_t)d * elem, (cuuint64_t)heads * d * elem};
-  cuuint32_t box[3] = {(cuuint32_t)(128 / elem), 1, (cuuint32_t)box_rows};
+  const int elem = key.elem, d = key.d;
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)key.heads, (cuuint64_t)key.rows};
+  cuuint64_t strides[2] = {(cuuint64_t)d * elem, (cuuint64_t)key.heads * d * elem};
+  cuuint32_t box[3] = {(cuuint32_t)(128 / elem), 1, (cuuint32_t)key.box_rows};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(out, elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
-                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   const_cast<void*>(key.ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SPPO_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  if (ctx->enc_cache.size() >= kEncCacheMax) ctx->enc_cache.clear();
-  ctx->enc_cache.emplace(key, *out);
   return SPPO_OK;
 }
 
-// The descriptor block of one launch.  Usage: open(), add() every map the
-// kernel reads (slot = index in the block), upload(stream) right before the
-// launch, close(stream) right after it.  Host-side failures before upload()
-// leave nothing enqueued.
+// Waits until every launch that may read the descriptor table has finished:
+// an event recorded on each stream that launched from it since the last
+// recycle (host wait), or the whole device if a stream cannot be recorded.
+sppo_status drain_desc_streams(sppo_ctx ctx) {
+  cudaEvent_t ev;
+  SPPO_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "descriptor recycle");
+  bool ok = true;
+  for (cudaStream_t st : ctx->desc_streams)
+    ok = ok && cudaEventRecord(ev, st) == cudaSuccess && cudaEventSynchronize(ev) == cudaSuccess;
+  cudaEventDestroy(ev);
+  if (!ok) {
+    cudaGetLastError();
+    SPPO_CUDA(cudaDeviceSynchronize(), "descriptor recycle");
+  }
+  for (int e = 0; e < kUploadEvents; ++e) ctx->up_live[e] = false;
+  ctx->desc_streams.clear();
+  return SPPO_OK;
+}
+
+// The descriptor set of one launch.  Usage: add() every map the kernel reads
+// (returns a request index), resolve(stream) once (uploads new maps, orders the
+// stream after pending uploads), then slot(index).  A failure leaves nothing
+// enqueued except, possibly, an upload of maps into free slots.
 struct DescBlock {
-  sppo_ctx ctx;
-  int b = -1, n = 0;
-  sppo_status open(sppo_ctx c) {
+  sppo_ctx ctx = nullptr;
+  std::vector<DescKey> keys;
+  std::vector<int> slots;
+  void open(sppo_ctx c) {
     ctx = c;
-    b = ctx->desc_block_next;
-    ctx->desc_block_next = (b + 1) % kDescBlocks;
-    n = 0;
-    // the staging and device block are free once the last kernel that used them finished
-    if (ctx->desc_ev_live[b]) SPPO_CUDA(cudaEventSynchronize(ctx->desc_ev[b]), "descriptor block reuse");
-    ctx->desc_ev_live[b] = false;
-    return SPPO_OK;
+    keys.clear();
+    slots.clear();
   }
-  sppo_status add(const void* ptr, int64_t rows, int heads, int d, int box_rows, int* slot, int elem = 2) {
-    if (n >= kDescBlockSlots) return fail(SPPO_E_UNSUPPORTED, "too many descriptors in one launch");
-    sppo_status s = encode_desc(ctx, ptr, rows, heads, d, box_rows, elem, &ctx->desc_host[b * kDescBlockSlots + n]);
-    if (s) return s;
-    *slot = n++;
-    return SPPO_OK;
+  int add(const void* ptr, int64_t rows, int heads, int d, int box_rows, int elem = 2) {
+    keys.push_back(DescKey{ptr, rows, heads, d, box_rows, elem});
+    return (int)keys.size() - 1;
   }
-  const void* table() const { return ctx->desc_dev + (size_t)b * kDescBlockSlots; }
-  sppo_status upload(cudaStream_t stream) {
-    SPPO_CUDA(cudaMemcpyAsync(ctx->desc_dev + (size_t)b * kDescBlockSlots, ctx->desc_host + (size_t)b * kDescBlockSlots,
-                              sizeof(CUtensorMap) * n, cudaMemcpyHostToDevice, stream),
-              "descriptor upload");
-    return SPPO_OK;
-  }
-  sppo_status close(cudaStream_t stream) {
-    SPPO_CUDA(cudaEventRecord(ctx->desc_ev[b], stream), "descriptor block event");
-    ctx->desc_ev_live[b] = true;
+  int slot(int i) const { return slots[i]; }
+  const void* table() const { return ctx->desc_dev; }
+  sppo_status resolve(cudaStream_t stream) {
+    if ((int)keys.size() > kDescCallMax) return fail(SPPO_E_UNSUPPORTED, "too many descriptors in one launch");
+    // pass 1: how many new maps (deduplicated); recycle first if they do not fit
+    std::vector<DescKey> fresh;
+    for (const DescKey& k : keys)
+      if (!ctx->desc_slot.count(k) && std::find(fresh.begin(), fresh.end(), k) == fresh.end()) fresh.push_back(k);
+    if (ctx->desc_next + (int)fresh.size() > kDescSlots) {
+      sppo_status s = drain_desc_streams(ctx);
+      if (s) return s;
+      ctx->desc_slot.clear();
+      ctx->desc_next = 0;
+    }
+    // pass 2: encode the new maps into consecutive slots of the host mirror
+    const int first = ctx->desc_next;
+    for (size_t f = 0; f < fresh.size(); ++f) {
+      sppo_status s = encode_desc(fresh[f], &ctx->desc_host[first + f]);
+      if (s) return s;
+    }
+    if (!fresh.empty()) {
+      // one upload of the new run, then its event (an event is re-recorded only after
+      // its previous upload is known complete, so a slot's generation check is exact)
+      const int e = ctx->up_next;
+      ctx->up_next = (e + 1) % kUploadEvents;
+      if (ctx->up_live[e]) SPPO_CUDA(cudaEventSynchronize(ctx->up_ev[e]), "descriptor upload event reuse");
+      SPPO_CUDA(cudaMemcpyAsync(ctx->desc_dev + first, ctx->desc_host + first, sizeof(CUtensorMap) * fresh.size(),
+                                cudaMemcpyHostToDevice, stream),
+                "descriptor upload");
+      SPPO_CUDA(cudaEventRecord(ctx->up_ev[e], stream), "descriptor upload event");
+      ++ctx->up_gen[e];
+      ctx->up_live[e] = true;
+      for (size_t f = 0; f < fresh.size(); ++f) {
+        const int sl = first + (int)f;
+        ctx->desc_slot[fresh[f]] = sl;
+        ctx->slot_up[sl] = sppo_ctx_s::SlotUpload{e, ctx->up_gen[e], stream, false};
+      }
+      ctx->desc_next = first + (int)fresh.size();
+    }
+    // pass 3: slots; order this stream after uploads issued on other streams
+    slots.resize(keys.size());
+    std::vector<int> waited;
+    for (size_t i = 0; i < keys.size(); ++i) {
+      const int sl = ctx->desc_slot[keys[i]];
+      slots[i] = sl;
+      sppo_ctx_s::SlotUpload& u = ctx->slot_up[sl];
+      if (u.done || u.stream == stream) continue;
+      if (u.gen != ctx->up_gen[u.ev] || cudaEventQuery(ctx->up_ev[u.ev]) == cudaSuccess) {
+        u.done = true;  // the event was re-recorded after a completed wait, or has completed
+        continue;
+      }
+      cudaGetLastError();  // cudaErrorNotReady from the query is not an error
+      if (std::find(waited.begin(), waited.end(), u.ev) == waited.end()) {
+        SPPO_CUDA(cudaStreamWaitEvent(stream, ctx->up_ev[u.ev], 0), "descriptor upload ordering");
+        waited.push_back(u.ev);
+      }
+    }
+    if (std::find(ctx->desc_streams.begin(), ctx->desc_streams.end(), stream) == ctx->desc_streams.end())
+      ctx->desc_streams.push_back(stream);
     return SPPO_OK;
   }
 };
@@ -373,14 +443,15 @@ sppo_status sppo_ctx_create(int device, sppo_ctx* out) {
       (e = cudaEventCreateWithFlags(&c->ev_prod, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&c->ev_cons, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming)) != cudaSuccess ||
-      (e = cudaMalloc(&c->desc_dev, sizeof(CUtensorMap) * kDescBlockSlots * kDescBlocks)) != cudaSuccess ||
-      (e = cudaHostAlloc(&c->desc_host, sizeof(CUtensorMap) * kDescBlockSlots * kDescBlocks, cudaHostAllocDefault)) !=
+      (e = cudaMalloc(&c->desc_dev, sizeof(CUtensorMap) * kDescSlots)) != cudaSuccess ||
+      (e = cudaHostAlloc(&c->desc_host, sizeof(CUtensorMap) * kDescSlots, cudaHostAllocDefault)) !=
           cudaSuccess) {
     sppo_ctx_destroy(c);
     return cuda_fail(e, "sppo_ctx_create");
   }
-  for (int b = 0; b < kDescBlocks; ++b)
-    if ((e = cudaEventCreateWithFlags(&c->desc_ev[b], cudaEventDisableTiming)) != cudaSuccess) {
+  c->slot_up.resize(kDescSlots);
+  for (int b = 0; b < kUploadEvents; ++b)
+    if ((e = cudaEventCreateWithFlags(&c->up_ev[b], cudaEventDisableTiming)) != cudaSuccess) {
     sppo_ctx_destroy(c);
     return cuda_fail(e, "sppo_ctx_create");
   }
@@ -415,8 +486,8 @@ sppo_status sppo_ctx_destroy(sppo_ctx c) {
   if (c->ev_prod) cudaEventDestroy(c->ev_prod);
   if (c->ev_cons) cudaEventDestroy(c->ev_cons);
   if (c->ev_copy) cudaEventDestroy(c->ev_copy);
-  for (int b = 0; b < kDescBlocks; ++b)
-    if (c->desc_ev[b]) cudaEventDestroy(c->desc_ev[b]);
+  for (int b = 0; b < kUploadEvents; ++b)
+    if (c->up_ev[b]) cudaEventDestroy(c->up_ev[b]);
   if (c->desc_dev) cudaFree(c->desc_dev);
   if (c->desc_host) cudaFreeHost(c->desc_host);
   if (c->trace) cudaFree(c->trace);
@@ -484,8 +555,9 @@ sppo_status sppo_attn_fwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
     a.p = p;
     a.n = kv->n;
     DescBlock db;
-    if ((s = db.open(ctx))) return s;
-    if ((s = db.add(q, p.q_len, p.heads, p.d, 128, &a.q_slot))) return s;
+    db.open(ctx);
+    const int rq = db.add(q, p.q_len, p.heads, p.d, 128);
+    std::vector<int> rk(kv->n), rv(kv->n);
     // kernel contract: the diagonal chunk (id == chunk), if present, is visited last
     std::vector<int> order;
     for (int c = 0; c < kv->n; ++c)
@@ -498,16 +570,17 @@ sppo_status sppo_attn_fwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
       const int64_t len = L->offsets[j + 1] - L->offsets[j];
       a.start[oc] = (int32_t)L->offsets[j];
       a.len[oc] = (int32_t)len;
-      int sk, sv;
-      if ((s = db.add(kv->k[c], len, p.heads, p.d, 128, &sk))) return s;
-      if ((s = db.add(kv->v[c], len, p.heads, p.d, 128, &sv))) return s;
-      a.slots.k[oc] = (uint16_t)sk;
-      a.slots.v[oc] = (uint16_t)sv;
+      rk[oc] = db.add(kv->k[c], len, p.heads, p.d, 128);
+      rv[oc] = db.add(kv->v[c], len, p.heads, p.d, 128);
+    }
+    if ((s = db.resolve(strm))) return s;
+    a.q_slot = db.slot(rq);
+    for (int oc = 0; oc < kv->n; ++oc) {
+      a.slots.k[oc] = (uint16_t)db.slot(rk[oc]);
+      a.slots.v[oc] = (uint16_t)db.slot(rv[oc]);
     }
     a.desc_table = db.table();
-    if ((s = db.upload(strm))) return s;
     e = launch_fwd_sm100(a, strm);
-    if (e == cudaSuccess && (s = db.close(strm))) return s;
   }
   if (e == cudaErrorNotSupported) return fail(SPPO_E_UNSUPPORTED, "this request is not implemented by the sm_100a kernels");
   if (e != cudaSuccess) return cuda_fail(e, "sppo_attn_fwd launch");
@@ -585,19 +658,17 @@ sppo_status sppo_attn_bwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
     sa.p = p;
     sa.n = kv->n;
     DescBlock db;
-    if ((s = db.open(ctx))) return s;
-    if ((s = db.add(q, p.q_len, p.heads, p.d, 128, &sa.q_slot))) return s;
-    if ((s = db.add(a->dout, p.q_len, p.heads, p.d, 128, &sa.do_slot))) return s;
-    if ((s = db.add(q, p.q_len, p.heads, p.d, 64, &sa.q64_slot))) return s;
-    if ((s = db.add(a->dout, p.q_len, p.heads, p.d, 64, &sa.do64_slot))) return s;
-    if ((s = db.add(a->dq_acc, p.q_len, p.heads, p.d, 128, &sa.dq_slot, 4))) return s;
+    db.open(ctx);
+    const int rq = db.add(q, p.q_len, p.heads, p.d, 128);
+    const int rdo = db.add(a->dout, p.q_len, p.heads, p.d, 128);
+    const int rq64 = db.add(q, p.q_len, p.heads, p.d, 64);
+    const int rdo64 = db.add(a->dout, p.q_len, p.heads, p.d, 64);
+    const int rdq = db.add(a->dq_acc, p.q_len, p.heads, p.d, 128, 4);
+    std::vector<int> rk(kv->n), rv(kv->n);
     int pairs = 0;
     for (int c = 0; c < kv->n; ++c) {
-      int sk, sv;
-      if ((s = db.add(kv->k[c], w.len[c], p.heads, p.d, 128, &sk))) return s;
-      if ((s = db.add(kv->v[c], w.len[c], p.heads, p.d, 128, &sv))) return s;
-      sa.slots.k[c] = (uint16_t)sk;
-      sa.slots.v[c] = (uint16_t)sv;
+      rk[c] = db.add(kv->k[c], w.len[c], p.heads, p.d, 128);
+      rv[c] = db.add(kv->v[c], w.len[c], p.heads, p.d, 128);
       sa.start[c] = w.start[c];
       sa.len[c] = w.len[c];
       sa.pair_base[c] = pairs;
@@ -606,11 +677,19 @@ sppo_status sppo_attn_bwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
       sa.dv[c] = a->dv_acc[c];
     }
     sa.pair_base[kv->n] = pairs;
+    if ((s = db.resolve(strm))) return s;
+    sa.q_slot = db.slot(rq);
+    sa.do_slot = db.slot(rdo);
+    sa.q64_slot = db.slot(rq64);
+    sa.do64_slot = db.slot(rdo64);
+    sa.dq_slot = db.slot(rdq);
+    for (int c = 0; c < kv->n; ++c) {
+      sa.slots.k[c] = (uint16_t)db.slot(rk[c]);
+      sa.slots.v[c] = (uint16_t)db.slot(rv[c]);
+    }
     sa.desc_table = db.table();
     if ((e = preprocess()) != cudaSuccess) return cuda_fail(e, "bwd preprocess");
-    if ((s = db.upload(strm))) return s;
     e = launch_bwd_sm100(sa, strm);
-    if (e == cudaSuccess && (s = db.close(strm))) return s;
   }
   if (e == cudaErrorNotSupported) return fail(SPPO_E_UNSUPPORTED, "this request is not implemented by the sm_100a kernels");
   if (e != cudaSuccess) return cuda_fail(e, "sppo_attn_bwd launch");

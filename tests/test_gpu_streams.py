@@ -78,12 +78,15 @@ def test_engine_step_on_side_stream(kind):
     ref = _ref(x)
     for _ in range(2):
         torch.cuda.synchronize()
-        k, v = dev["k"].clone(), dev["v"].clone()
+        # inputs are produced (and complete) before the spin: only the step's own
+        # torch-side work may land on the held stream
+        q, k, v = dev["q"].clone(), dev["k"].clone(), dev["v"].clone()
+        torch.cuda.synchronize()
         torch.cuda._sleep(SPIN)  # on the current (default) stream
         if kind == "step":
             out = eng.step(dev["q"], k, v, dev["do"], stream=side)
         elif kind == "offload":
-            eng.step_offload(dev["q"].clone(), k, v, dev["do"], [0.5] * (N - 1) + [0.0], stream=side, poison=True)
+            eng.step_offload(q, k, v, dev["do"], [0.5] * (N - 1) + [0.0], stream=side, poison=True)
         elif kind == "kv_stream":
             eng.step_kv_stream(dev["q"], k, v, dev["do"], hot=2, window=2, stream=side, poison=True)
         else:

@@ -196,10 +196,11 @@ def test_sampled_rows_and_key_grads_match_dense():
     np.testing.assert_allclose(r["lse"], g["lse"][:, rows], atol=1e-12)
     np.testing.assert_allclose(r["delta"], g["delta"][:, rows], atol=1e-12)
     np.testing.assert_allclose(r["dq"], g["dq"][rows], atol=1e-12)
-    keys = [250, 251, 299]
-    kg = oracle.sampled_key_grads(x["q"], x["k"], x["v"], x["do"], keys, row_block=17)
-    np.testing.assert_allclose(kg["dk"], g["dk"][keys], atol=1e-12)
-    np.testing.assert_allclose(kg["dv"], g["dv"][keys], atol=1e-12)
+    # late keys, and early keys (rows of blocks that precede some keys: P = 0 there)
+    for keys, rb in (([250, 251, 299], 17), ([0, 1, 16, 17, 100, 299], 7), ([3, 150], 300), ([299], 1)):
+        kg = oracle.sampled_key_grads(x["q"], x["k"], x["v"], x["do"], keys, row_block=rb)
+        np.testing.assert_allclose(kg["dk"], g["dk"][keys], atol=1e-12)
+        np.testing.assert_allclose(kg["dv"], g["dv"][keys], atol=1e-12)
     r1 = oracle.sampled_rows(x["q"], x["k"], x["v"], [5], heads=[1])
     np.testing.assert_allclose(r1["o"][:, 0], g["o"][[5], 1], atol=1e-12)
 
