@@ -642,7 +642,7 @@ def run_layer(args, cfg, ws, rank, local):
     partition the heads (tensor parallelism: column / row-parallel projections,
     NCCL all-reduce of the partial sums, engine_layer tp=...): the total work is
     fixed (strong scaling), value = the whole layer's FLOPs / max-over-ranks time."""
-    from paper_2503_10377_b200 import engine_layer, sppo
+    from paper_2503_10377_b200 import engine_layer, msp, sppo
     import synth
 
     dev = torch.device("cuda", local)
@@ -704,10 +704,40 @@ def run_layer(args, cfg, ws, rank, local):
     pipe = {"note": "MODEL from this run's measured per-chunk layer fwd/bwd times (1 layer per stage); "
                     "multi-GPU execution not measured (one GPU in this environment)",
             "F_ms": round(F, 3)}
+    # MSP: bubble-adjacent chunks tensor-parallel over the
+    # stage's Left-SP / Right-SP range (msp.py).  Per-rank times of a g-way shard of
+    # this layer (heads / g, MLP columns / g) are MEASURED here for g | heads (one
+    # rank's compute; the range's all-reduces not included); other g: t_1 / g.
+    shard = {}
+    if ws == 1 and not args.no_msp:
+        for g in (2, 4, 8):
+            if heads % g:
+                continue
+            sl = engine_layer.ChunkedLayer(ctx, H, heads, offsets, engine_layer.shard_params(params, H, heads, 0, g),
+                                           device=dev, tp=(0, g, False))
+            sl.step(io["x"], io["dz"], stream)
+            sl.timing, sl.events = True, {"fwd": [], "bwd": []}
+            sl.step(io["x"], io["dz"], stream)
+            torch.cuda.synchronize()
+            shard[g] = (sl.chunk_ms("fwd"), list(reversed(sl.chunk_ms("bwd"))))
+            del sl
     for pp in (2, 4, 8):
         T = sppo.pipeline_makespan(pp, t_fwd, t_bwd)
         pipe[f"pp{pp}"] = {"makespan_ms": round(T, 3), "bubble_ratio": round((T - F) / F, 4),
                            "uniform_formula": round(sppo.pipeline_bubble(pp, N), 4)}
+        if shard:
+            tf = {1: t_fwd, **{g: (shard[g][0] if g in shard else [x / g for x in t_fwd]) for g in range(2, pp + 1)}}
+            tb = {1: t_bwd, **{g: (shard[g][1] if g in shard else [x / g for x in t_bwd]) for g in range(2, pp + 1)}}
+            Tm = msp.msp_makespan(pp, N, offsets, tf, tb, msp=True)
+            Ti = msp.msp_makespan(pp, N, offsets, t_fwd, t_bwd, msp=True)
+            pipe[f"pp{pp}"]["msp"] = {"makespan_ms": round(Tm, 3), "bubble_ratio": round((Tm - F) / F, 4),
+                                      "speedup_vs_plain": round(T / Tm, 4),
+                                      "makespan_perfect_split_ms": round(Ti, 3)}
+    if shard:
+        pipe["shard_efficiency"] = {f"g{g}": round(F / (g * (sum(f) + sum(b))), 4) for g, (f, b) in shard.items()}
+        pipe["msp_note"] = ("MSP plan (msp.MSPPlan list schedule) with this run's per-chunk times; a range of g GPUs "
+                            "takes the measured per-rank time of a g-way shard (g | heads) or t_1 / g; "
+                            "all-reduces and phase-boundary K/V moves not modeled")
     lay.gemm_events = None
 
     # Type-1 activation offload with sequence-aware alpha vs the paper's fixed full offload
@@ -815,7 +845,7 @@ def run_layer_pool(args, cfg, ws, rank, local):
     all-resident step does not fit (e.g. C3's 1M tokens at hidden 4096).  Warm-up
     steps 1-2 run alpha = 1, step 2 measures the per-chunk forward times; alpha is then
     the sequence-aware plan.  value = FLOPs / offloaded step time."""
-    from paper_2503_10377_b200 import engine_layer, sppo
+    from paper_2503_10377_b200 import engine_layer, msp, sppo
     import synth
 
     dev = torch.device("cuda", local)
@@ -979,6 +1009,7 @@ def main():
     ap.add_argument("--chunks", type=int, default=0, help="override the config's N (tests)")
     ap.add_argument("--o-digest", action="store_true",
                     help="add sha256 of the (gathered) forward output O to the line (sharded == unsharded check)")
+    ap.add_argument("--no-msp", action="store_true", help="layer workload: skip the MSP shard timings")
     ap.add_argument("--no-c3", action="store_true",
                     help="skip the bounded C3 (1M tokens, the north-star target) sub-measurement of the C2 line")
     args = ap.parse_args()

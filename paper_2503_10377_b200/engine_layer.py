@@ -175,7 +175,7 @@ class ChunkedLayer:
         """Sum over the tensor-parallel ranks, in place (no-op without TP).  NCCL:
         stream-ordered on `strm` (the current stream inside step); otherwise
         (gloo, tests) host-staged."""
-        if self.tp_size == 1:
+        if self.tp_size == 1 or self.tp_group is False:  # False: a timing-only shard (bench MSP model)
             return
         import torch.distributed as dist
         st = strm if isinstance(strm, torch.cuda.Stream) else torch.cuda.current_stream()

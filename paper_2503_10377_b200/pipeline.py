@@ -18,9 +18,8 @@ chunk i+1 is posted before chunk i's compute so the transfer overlaps it.
 Every arithmetic step runs in the layers' ABI calls (engine_layer.ChunkedLayer);
 this module only sequences them and moves bytes.
 
-MSP (Left-SP / Steady / Right-SP) is provided as the plan helper
-sppo_msp_phases; executing the SP phases needs the bubble-adjacent stages'
-weights on every GPU of the SP range and is not built.
+MSP (Left-SP / Steady / Right-SP) is executed by msp.py: the same
+stages, with bubble-adjacent chunks tensor-parallel over the stage's SP range.
 """
 
 from __future__ import annotations
