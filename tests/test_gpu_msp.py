@@ -47,7 +47,7 @@ def _worker(rank, world, port, S, H, heads, N, out):
         torch.cuda.synchronize()
         res[use] = {k: (v.float().cpu().numpy() if torch.is_tensor(v) else {n: g.cpu().numpy() for n, g in v.items()})
                     for k, v in r.items()}
-        res[(use, "tasks")] = sum(1 for t in ex.log if t[0] in "FB" and t[1] != rank)
+        res[(use, "tasks")] = sum(1 for t in ex.log if t[0] in "FB" and t[1] != rank and rank in ex.plan.group(t[1], t[2]))
         del ex
     ctx.sync()
     np.save(os.path.join(out, f"r{rank}.npy"), res, allow_pickle=True)
