@@ -77,6 +77,7 @@ struct Sm100Fwd {
   FwdParams p;
   const void* desc_table;  // device array of CUtensorMap
   int32_t q_slot;          // descriptor slot of Q_i
+  int32_t o_slot;          // descriptor slot of O_i (bf16, 128-row boxes; TMA store on LAST), -1 if none
   int32_t n;               // window size
   int32_t start[kMaxWindow];
   int32_t len[kMaxWindow];

@@ -406,15 +406,18 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
           p.l[(size_t)head * p.q_len + row] = l;
         }
       }
-      const float inv = 1.f / l;
-      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + ((size_t)row * p.heads + head) * HD;
+      if (p.last) {
+        // O = acc / l in bf16 into the tile's Q buffer (free: its last S MMA completed
+        // before the last softmax), SW128 layout, then two TMA stores (coalesced;
+        // rows >= q_len clipped by the tensor map)
+        const float inv = 1.f / l;
+        uint8_t* qb = sQ + t * kTileBytes;
 #pragma unroll
-      for (int cb = 0; cb < 4 && p.last; ++cb) {
-        uint32_t o[32];
-        tmem_ld32(sO + cb * 32, o);
-        tmem_wait_ld();
-        if (ok) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + cb * 32);
+        for (int cb = 0; cb < 4; ++cb) {
+          uint32_t o[32];
+          tmem_ld32(sO + cb * 32, o);
+          tmem_wait_ld();
+          uint8_t* box = qb + (cb >> 1) * kHalf;
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
             uint4 w;
@@ -422,8 +425,18 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
             w.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
             w.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
             w.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
-            dst[v] = w;
+            const int chunk16 = (cb & 1) * 4 + v;  // 16-byte chunk within the 128-byte box row
+            *reinterpret_cast<uint4*>(box + row_in_tile * 128 + ((chunk16 ^ (row_in_tile & 7)) << 4)) = w;
           }
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(9 + t, 128);  // the tile's four softmax warps staged their rows
+        if (wq == 0 && lane == 0) {
+          const CUtensorMap* mo = tmap(a, a.o_slot);
+          tma_store_3d(mo, qb, 0, head, r0 + t * BM);
+          tma_store_3d(mo, qb + kHalf, 64, head, r0 + t * BM);
+          bulk_commit();
+          bulk_wait_read<0>();
         }
       }
       if (ok && p.last) p.lse[(size_t)head * p.q_len + row] = (m_used + __log2f(l)) * 0.6931471805599453f;
@@ -434,13 +447,15 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+
+
 }  // namespace
 
 cudaError_t launch_fwd_sm100(const Sm100Fwd& a, cudaStream_t s) {
   if (a.p.d != HD) return cudaErrorNotSupported;
+  dim3 grid((a.p.q_len + 2 * BM - 1) / (2 * BM), a.p.heads);
   cudaError_t e = ensure_smem_attr((const void*)fwd_kernel, kSmemBytes);
   if (e != cudaSuccess) return e;
-  dim3 grid((a.p.q_len + 2 * BM - 1) / (2 * BM), a.p.heads);
   fwd_kernel<<<grid, kThreads, kSmemBytes, s>>>(a);
   return cudaGetLastError();
 }

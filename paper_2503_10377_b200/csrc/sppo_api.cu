@@ -557,6 +557,7 @@ sppo_status sppo_attn_fwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
     DescBlock db;
     db.open(ctx);
     const int rq = db.add(q, p.q_len, p.heads, p.d, 128);
+    const int ro = last ? db.add(o, p.q_len, p.heads, p.d, 128) : -1;
     std::vector<int> rk(kv->n), rv(kv->n);
     // kernel contract: the diagonal chunk (id == chunk), if present, is visited last
     std::vector<int> order;
@@ -575,6 +576,7 @@ sppo_status sppo_attn_fwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
     }
     if ((s = db.resolve(strm))) return s;
     a.q_slot = db.slot(rq);
+    a.o_slot = last ? db.slot(ro) : -1;
     for (int oc = 0; oc < kv->n; ++oc) {
       a.slots.k[oc] = (uint16_t)db.slot(rk[oc]);
       a.slots.v[oc] = (uint16_t)db.slot(rv[oc]);

@@ -184,21 +184,22 @@ class MSPPlan:
         return self.group(task[1], task[2]) if task[0] in ("F", "B") else self.participants(task)
 
     def _order(self):
-        """Critical-path list scheduling: repeatedly take the ready task with the
-        longest remaining path to the end of the step (its bottom level; ties by
-        stage, kind, chunk) and start it as early as its predecessors and the
-        ranks it occupies allow.  The walk order is the tasks sorted by start
+        """List scheduling of the task graph: repeatedly take the ready task of
+        highest priority and start it as early as its predecessors and the ranks it
+        occupies allow.  Three priority rules are tried — critical path (longest
+        remaining path to the end), earliest feasible start, and pipeline order
+        (forward: lower stage first; backward: higher stage first) — and the
+        schedule with the smallest makespan is kept (deterministic: every rank
+        computes the same one).  The walk order is the tasks sorted by start
         (scheduling sequence for ties, which respects every dependency)."""
         deps = self._deps()
         succ = {t: [] for t in deps}
-        indeg = {t: len(d) for t, d in deps.items()}
         for t, d in deps.items():
             for u in d:
                 succ[u].append(t)
+        indeg0 = {t: len(d) for t, d in deps.items()}
         # bottom levels (longest path to exit, including the task itself)
-        level = {}
-        topo, stack = [], [t for t, n in indeg.items() if n == 0]
-        cnt = dict(indeg)
+        topo, stack, cnt = [], [t for t, n in indeg0.items() if n == 0], dict(indeg0)
         while stack:
             t = stack.pop()
             topo.append(t)
@@ -207,26 +208,45 @@ class MSPPlan:
                 if cnt[u] == 0:
                     stack.append(u)
         assert len(topo) == len(deps), "task graph has a cycle"
+        level = {}
         for t in reversed(topo):
             level[t] = self.cost(t) + max([level[u] for u in succ[t]] + [0.0])
-        end, free = {}, [0.0] * self.PP
-        ready = [t for t, n in indeg.items() if n == 0]
-        seq = []
-        self.start = {}
-        while ready:
-            t = max(ready, key=lambda u: (level[u], -u[1] if u[0] == "F" else u[1], -"FLSRBSLRSG".find(u[0]), -u[2]))
-            ready.remove(t)
-            st = max([end[u] for u in deps[t]] + [free[r] for r in self.busy(t)] + [0.0])
-            self.start[t] = st
-            end[t] = st + self.cost(t)
-            for r in self.busy(t):
-                free[r] = end[t]
-            seq.append(t)
-            for u in succ[t]:
-                indeg[u] -= 1
-                if indeg[u] == 0:
-                    ready.append(u)
-        self.end = end
+        kind_rank = lambda u: "FLSRBSLRSG".find(u[0])  # noqa: E731
+
+        def schedule(rule):
+            indeg = dict(indeg0)
+            end, free, start, seq = {}, [0.0] * self.PP, {}, []
+            ready = [t for t, n in indeg.items() if n == 0]
+
+            def est(u):
+                return max([end[v] for v in deps[u]] + [free[r] for r in self.busy(u)] + [0.0])
+            while ready:
+                if rule == "critical":
+                    t = max(ready, key=lambda u: (level[u], -u[1] if u[0] == "F" else u[1], -kind_rank(u), -u[2]))
+                elif rule == "earliest":
+                    t = min(ready, key=lambda u: (est(u), -level[u], kind_rank(u), u[1], u[2]))
+                else:  # pipeline order
+                    t = min(ready, key=lambda u: (0 if u[0] in ("F", "LS", "SR") else 1,
+                                                  u[1] if u[0] in ("F", "LS", "SR") else -u[1],
+                                                  u[2] if u[0] in ("F", "LS", "SR") else -u[2], kind_rank(u)))
+                ready.remove(t)
+                st = est(t)
+                start[t], end[t] = st, st + self.cost(t)
+                for r in self.busy(t):
+                    free[r] = end[t]
+                seq.append(t)
+                for u in succ[t]:
+                    indeg[u] -= 1
+                    if indeg[u] == 0:
+                        ready.append(u)
+            return max(end.values()), start, end, seq
+
+        best = None
+        for rule in ("critical", "earliest", "pipeline"):
+            res = schedule(rule)
+            if best is None or res[0] < best[0] - 1e-12:
+                best = res + (rule,)
+        _, self.start, self.end, seq, self.rule = best
         pos = {t: n for n, t in enumerate(seq)}
         return sorted(seq, key=lambda t: (self.start[t], pos[t]))
 
