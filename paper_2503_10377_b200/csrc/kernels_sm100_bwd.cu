@@ -62,6 +62,11 @@ constexpr uint32_t kOffDS = kOffOB + kBox;        // dS [128 keys][128 q] (two q
 #define SPPO_DQ_RED_PIECES 0  // measured: 1 piece -> bwd 841, 2 -> 775 vs 1017 TF/s (L2/LSU bound)
 #endif
 constexpr int kDqRedPieces = SPPO_DQ_RED_PIECES;  // of the 4 dQ pieces, sent by red.global.add.v4.f32
+// Two staging buffers, one issuing thread.  Measured alternatives (profiles/r02):
+// 4 buffers with each reducer warp issuing its own piece -> bwd 950-955 vs 1037-1039
+// TF/s; the 4 pieces as ONE 4-D reduce (box {32, 128, 4, 1}) -> 937 vs 1049: a 64 KB
+// reduce-add takes ~3600 cycles to drain from shared memory (~18 B/clk per SM), i.e.
+// the dQ path is bound by the L2 reduction rate, not by TMA issue.
 constexpr int kDqBufs = 2;
 #ifndef SPPO_EPI_RED
 #define SPPO_EPI_RED 1  // measured: bwd +3 % at C2, +9 % at 2K chunks vs load-add-store
