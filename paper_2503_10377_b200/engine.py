@@ -58,15 +58,22 @@ class ChunkedAttention:
         # resident step(): forward chunks are independent (chunk i reads only inputs), so
         # consecutive forward launches may alternate between two streams and the next one
         # fills the SMs the previous one's last wave leaves idle.  Measured: worth it
-        # when a launch is a few waves (C2 per-GPU shares at 2-8 GPUs: +5 %), harmful when
-        # it is many (C3, 14 waves: two kernels sweeping different K/V positions, -11 %
-        # forward).  Default: two streams below 8 waves of CTAs per launch.
+        # when a launch is a few waves and its K/V sweep is short (C2 per-GPU shares at
+        # 2-8 GPUs: +5 %), harmful when two concurrent kernels sweep long, different K/V
+        # ranges (C3, 14 waves, 17 GB of K/V: -11 % forward; the C5 per-GPU share,
+        # 3.5 waves but 17 GB: -10 %, profiles/r02).  Default: two streams below 8
+        # waves of CTAs per launch and at most 4 GB of K/V behind the last chunk.
+        # Grouped KV streaming shares ONE window between the concurrent launches, so
+        # there the wave count alone decides (C5 share: -2 % step time).
+        smax = max(layout.chunk_len(i) for i in range(layout.num_chunks))
+        ctas = -(-smax // 256) * layout.heads  # fwd_kernel: 2 Q tiles of 128 rows per CTA
+        sms = torch.cuda.get_device_properties(torch.device(device)).multi_processor_count \
+            if torch.cuda.is_available() else 148
+        self._few_waves = ctas < 8 * sms
         if fwd_streams is None:
-            smax = max(layout.chunk_len(i) for i in range(layout.num_chunks))
-            ctas = -(-smax // 256) * layout.heads  # fwd_kernel: 2 Q tiles of 128 rows per CTA
-            sms = torch.cuda.get_device_properties(torch.device(device)).multi_processor_count \
-                if torch.cuda.is_available() else 148
-            fwd_streams = 2 if ctas < 8 * sms else 1
+            kv_bytes = layout.offsets[-1] * layout.heads * layout.head_dim * 2 * \
+                torch.tensor([], dtype=DTYPES[layout.dtype]).element_size()
+            fwd_streams = 2 if (self._few_waves and kv_bytes <= 4e9) else 1
         self.fwd_streams = fwd_streams
         self._side = None
         # instrumentation (tools/offload_timeline.py): when a list, every compute call
@@ -537,6 +544,17 @@ class ChunkedAttention:
                     ks_all = [self.rows(k, j) for j in ids]
                     vs_all = [self.rows(v, j) for j in ids]
                 stats["windows"] += 1
+                # the group's forwards of one window are independent (own Q, carry and
+                # outputs; shared K/V window): with few waves per launch they alternate
+                # between two streams so one launch fills the other's last wave; the
+                # side stream joins back before the window's ring slot is reused
+                two = kind == "fwd" and len(C) > 1 and self._few_waves
+                if two:
+                    if self._side is None:
+                        self._side = torch.cuda.Stream(device=self.device)
+                    fork = torch.cuda.Event()
+                    fork.record(strm)
+                    self._side.wait_event(fork)
                 for gi, i in enumerate(C):
                     sel = [c for c, j in enumerate(ids) if j <= i]
                     if not sel:
@@ -550,7 +568,8 @@ class ChunkedAttention:
                     if kind == "fwd":
                         self.ctx.attn_fwd(L, i, self.rows(q, i), wids, ks, vs, flags=flags,
                                           state=None if len(my) == 1 else (sc["o_acc"][:s], sc["m"][:s * h], sc["l"][:s * h]),
-                                          o=self.rows(self.o, i), lse=self.lse_view(i), stream=strm)
+                                          o=self.rows(self.o, i), lse=self.lse_view(i),
+                                          stream=self._side if (two and gi % 2) else strm)
                         self.launches += 1
                     else:
                         has_i = i in wids
@@ -561,6 +580,10 @@ class ChunkedAttention:
                                           dq=self.rows(self.dq, i), dk=self.rows(self.dk, i) if has_i else None,
                                           dv=self.rows(self.dv, i) if has_i else None, flags=flags, stream=strm)
                         self.launches += 1 + (flags & sppo.SPPO_FIRST != 0) + (flags & sppo.SPPO_LAST != 0)
+                if two:
+                    join = torch.cuda.Event()
+                    join.record(self._side)
+                    strm.wait_event(join)
             if kind == "fwd":
                 last_ev = None
                 for i in C:
