@@ -66,7 +66,11 @@ constexpr int kDqRedPieces = SPPO_DQ_RED_PIECES;  // of the 4 dQ pieces, sent by
 // 4 buffers with each reducer warp issuing its own piece -> bwd 950-955 vs 1037-1039
 // TF/s; the 4 pieces as ONE 4-D reduce (box {32, 128, 4, 1}) -> 937 vs 1049: a 64 KB
 // reduce-add takes ~3600 cycles to drain from shared memory (~18 B/clk per SM), i.e.
-// the dQ path is bound by the L2 reduction rate, not by TMA issue.
+// the dQ path is bound by the L2 reduction rate, not by TMA issue.  Summing the
+// pair's two partials first (CTA r keeps d-columns [64r, +64) and stores the other
+// 64 into the peer's smem over DSMEM, halving the L2 reduce bytes) measured bwd
+// 612-627 (row-swizzled remote stores) / 720 (coalesced [chunk][row] layout) vs
+// 1032-1036 TF/s: thread stores to the peer's shared memory moved ~4-5 B/clk.
 constexpr int kDqBufs = 2;
 #ifndef SPPO_EPI_RED
 #define SPPO_EPI_RED 1  // measured: bwd +3 % at C2, +9 % at 2K chunks vs load-add-store
