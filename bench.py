@@ -68,12 +68,12 @@ def load_peaks():
 
 def ncu_traffic(kernel):
     """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
-    --set full capture (profiles/r01/ncu_traffic.json), or None."""
-    p = os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")
+    --set full capture (profiles/r02/ncu_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")
     try:
         d = json.load(open(p))[kernel]
         return {"bytes": d["dram_read_bytes"] + d["dram_write_bytes"], "launch": d["launch"],
-                "source": "profiles/r01/ncu_traffic.json (ncu --set full, one launch)"}
+                "source": "profiles/r02/ncu_traffic.json (ncu --set full, one launch)"}
     except Exception:
         return None
 

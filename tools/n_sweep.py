@@ -2,7 +2,7 @@
 attention layer split into N = 1 .. 128 chunks, fwd+bwd TFLOP/s per N (the
 subsequence-length trade-off of P:276 / P:289-294 for the attention layer:
 more chunks = smaller launches, more diagonal-tile waste and tails).
-usage: python tools/n_sweep.py > profiles/r01/n_sweep.json"""
+usage: python tools/n_sweep.py > profiles/r02/n_sweep.json"""
 import json
 import os
 import sys
@@ -23,16 +23,20 @@ for N in (1, 2, 4, 8, 16, 32, 64, 128):
     for _ in range(3):
         eng.step(x["q"], x["k"], x["v"], x["do"])
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(3):
-        eng.step(x["q"], x["k"], x["v"], x["do"])
-    e1.record()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+    for r in range(3):
+        ev[2 * r].record()
+        eng.step(x["q"], x["k"], x["v"], x["do"], mark=ev[2 * r + 1])
+    ev[6].record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / 3
-    fl = 14 * d * h * sppo.causal_pairs(off)
+    ms = ev[0].elapsed_time(ev[6]) / 3
+    fwd_ms = sum(ev[2 * r].elapsed_time(ev[2 * r + 1]) for r in range(3)) / 3
+    pairs = sppo.causal_pairs(off)
+    fl = 14 * d * h * pairs
     res.append({"N": N, "chunk_len": S // N, "ms_per_step": round(ms, 2), "tflops": round(fl / ms / 1e9, 1),
-                "launches_per_step": eng.launches // 6})
+                "fwd_tflops": round(4 * d * h * pairs / fwd_ms / 1e9, 1),
+                "bwd_tflops": round(10 * d * h * pairs / (ms - fwd_ms) / 1e9, 1),
+                "fwd_streams": eng.fwd_streams, "launches_per_step": eng.launches // 6})
     del eng
     torch.cuda.empty_cache()
 print(json.dumps({"config": "C2 shape: 32 heads, d=128, S=131072, bf16, resident; 3 warm-up + 3 timed steps",
