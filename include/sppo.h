@@ -30,7 +30,7 @@
  * FP32 reference path, d <= 128).
  *
  * Ownership: the caller owns every device and host tensor passed in.  The
- * library owns only the ctx (copy streams, events, TMA descriptor ring,
+ * library owns only the ctx (copy streams, events, TMA descriptor table,
  * window-coverage state) and host buffers returned by sppo_host_alloc.
  * No call frees caller memory.
  *
@@ -42,11 +42,13 @@
  *
  * Streams/events are passed as void* holding a cudaStream_t / cudaEvent_t
  * (NULL stream = legacy default stream).  No call synchronises the device
- * unless its name says so.  (sppo_attn_fwd / sppo_attn_bwd may wait on the
- * host for the kernel launched 128 compute calls earlier on the same ctx:
- * each launch owns one block of a ring of TMA-descriptor tables, uploaded on
- * the launch stream itself, and a block is reused only after its kernel
- * completed.)
+ * unless its name says so.  Descriptor table: the TMA tensor maps of every
+ * (pointer, shape) a call reads live in one persistent device table of the ctx
+ * (16384 maps), uploaded once, on first use, on the launch stream; a later call
+ * on another stream waits on that upload's event.  When a call's new maps do
+ * not fit, the table is recycled first: sppo_attn_fwd / sppo_attn_bwd then wait
+ * on the host until every stream that launched from the ctx since the last
+ * recycle has drained (rare: thousands of distinct buffers or chunk views).
  */
 #ifndef SPPO_H_
 #define SPPO_H_

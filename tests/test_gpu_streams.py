@@ -168,3 +168,31 @@ def test_many_distinct_buffers_no_device_sync():
     for *_, o in outs[1:]:
         assert torch.equal(o, first)  # forward bitwise deterministic (reading L12)
     ctx.close()
+
+
+def test_descriptor_table_recycles_mid_step():
+    """256 chunks of 128 tokens, every window one launch: one step needs ~66K
+    distinct tensor maps (each chunk's K / V view in every later window), four
+    times the 16384-slot descriptor table, so the table is recycled several times
+    while earlier launches are still in flight (include/sppo.h "Descriptor
+    table"; ADVICE r1).  The result must still equal the oracle."""
+    from paper_2503_10377_b200 import engine, sppo
+    S, h, N = 256 * 128, 1, 256
+    x = make_inputs(S, range(h), 128, seed=75, dtype=torch.bfloat16)
+    dev = {k: v.cuda() for k, v in x.items()}
+    ctx = sppo.Context(0)
+    eng = engine.ChunkedAttention(ctx, sppo.Layout(h, 128, sppo.partition_equal(S, N)))
+    for _ in range(2):  # the second step starts from a table the first one left full
+        out = eng.step(dev["q"], dev["k"], dev["v"], dev["do"])
+    torch.cuda.synchronize()
+    ctx.sync()
+    rows = [0, 127, 128, 4095, 16383, 16384, S - 129, S - 1]
+    xn = {k: v.double().numpy() for k, v in x.items()}
+    ref = oracle.sampled_rows(xn["q"], xn["k"], xn["v"], rows, do=xn["do"])
+    np.testing.assert_allclose(out["o"][rows].double().cpu().numpy(), ref["o"], **O_TOL)
+    np.testing.assert_allclose(out["dq"][rows].double().cpu().numpy(), ref["dq"], **G_TOL)
+    keys = sorted(set(range(S - 300, S, 37)) | {S - 1})
+    kg = oracle.sampled_key_grads(xn["q"], xn["k"], xn["v"], xn["do"], keys, row_block=128)
+    np.testing.assert_allclose(out["dk"][keys].double().cpu().numpy(), kg["dk"], **G_TOL)
+    np.testing.assert_allclose(out["dv"][keys].double().cpu().numpy(), kg["dv"], **G_TOL)
+    ctx.close()
