@@ -135,6 +135,24 @@ sppo_status sppo_attn_fwd(sppo_ctx ctx, const sppo_layout* layout, int32_t chunk
                           const void* q, const sppo_kv_set* kv, int32_t flags,
                           const sppo_fwd_state* st, void* o, float* lse, void* stream);
 
+/*
+ * sppo_attn_fwd_chunks — forward of chunks i0..i1-1 in ONE launch, each over its
+ *   whole prior-KV set (one window, FIRST|LAST; same results as sppo_attn_fwd
+ *   per chunk).  The Q tiles of all the chunks form one grid ordered longest
+ *   chunk first (the last wave holds the shortest work), and their CTAs sweep
+ *   the shared K/V from position 0 upward together — the per-chunk launches'
+ *   wave tails and launch gaps disappear (SURVEY §8(e) "persistent scheduler").
+ *   Chunk i's queries still see only keys t <= p.  bf16 only
+ *   (SPPO_E_UNSUPPORTED for fp32: use sppo_attn_fwd per chunk).
+ *   q, o : HOST arrays of i1 - i0 DEVICE pointers, chunk i0 + k at [k], each [s_i, heads, d]
+ *   lse  : HOST array of i1 - i0 DEVICE pointers, each [heads, s_i] fp32
+ *   kv   : ids exactly 0..i1-1 in ascending order (SPPO_E_ARG otherwise)
+ * Enqueued on `stream`; returns after enqueue.
+ */
+sppo_status sppo_attn_fwd_chunks(sppo_ctx ctx, const sppo_layout* layout, int32_t i0, int32_t i1,
+                                 const void* const* q, const sppo_kv_set* kv, void* const* o, float* const* lse,
+                                 void* stream);
+
 /* Backward tensors of chunk i.  All DEVICE pointers. */
 typedef struct {
   const void* o;          /* [s_i, heads, d] dtype: forward output O_i              */

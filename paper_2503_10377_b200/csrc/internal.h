@@ -82,6 +82,13 @@ struct Sm100Fwd {
   int32_t start[kMaxWindow];
   int32_t len[kMaxWindow];
   TmaSlots slots;
+  // multi-chunk launch (nq > 0, sppo_attn_fwd_chunks): Q chunks q0..q0+nq-1 (window
+  // index = chunk id, window = chunks 0..q0+nq-1, FIRST|LAST), blocks ordered longest
+  // chunk first: block_base[k] = first block of chunk q0+nq-1-k
+  int32_t nq, q0;
+  int32_t block_base[kMaxWindow + 1];
+  uint16_t qslots[kMaxWindow], oslots[kMaxWindow];  // by chunk - q0
+  float* lses[kMaxWindow];
 };
 
 struct Sm100Bwd {

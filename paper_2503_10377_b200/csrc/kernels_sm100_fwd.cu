@@ -90,20 +90,36 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
   const FwdParams& p = a.p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int head = blockIdx.y;
-  const int r0 = blockIdx.x * (2 * BM);  // first local row of Q tile 0
+  // ---- this CTA's Q chunk: the call's chunk, or (multi-chunk launch) the chunk whose
+  // block range holds blockIdx.x — longest chunks first, so the last wave is short
+  int q_start = p.q_start, q_len = p.q_len, q_slot = a.q_slot, o_slot = a.o_slot, win_n = a.n;
+  float* lse_out = p.lse;
+  int r0 = blockIdx.x * (2 * BM);  // first local row of Q tile 0
+  if (a.nq > 0) {
+    int k = 0;
+    while (k + 1 < a.nq && a.block_base[k + 1] <= (int)blockIdx.x) ++k;
+    const int c = a.q0 + a.nq - 1 - k;  // chunk id = its window index
+    q_start = a.start[c];
+    q_len = a.len[c];
+    q_slot = a.qslots[c - a.q0];
+    o_slot = a.oslots[c - a.q0];
+    lse_out = a.lses[c - a.q0];
+    win_n = c + 1;  // later chunks of the window are invisible to these rows
+    r0 = ((int)blockIdx.x - a.block_base[k]) * (2 * BM);
+  }
 
   // ---- per-CTA tile counts (the diagonal chunk is last in the window)
   int T[2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
     const int first_row = r0 + t * BM;
-    if (first_row >= p.q_len) {
+    if (first_row >= q_len) {
       T[t] = 0;
       continue;
     }
-    const int last_pos = p.q_start + min(first_row + BM, p.q_len) - 1;
+    const int last_pos = q_start + min(first_row + BM, q_len) - 1;
     int n = 0;
-    for (int c = 0; c < a.n; ++c) {
+    for (int c = 0; c < win_n; ++c) {
       const int st = a.start[c], ln = a.len[c];
       const int hi = min(st + ln - 1, last_pos);  // last visible key of this chunk
       if (hi >= st) n += (hi - st) / BN + 1;
@@ -146,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
-      const CUtensorMap* mq = tmap(a, a.q_slot);
+      const CUtensorMap* mq = tmap(a, q_slot);
       prefetch_tmap(mq);
       mbar_arrive_expect_tx(&bars.q_full, 2 * kTileBytes);
 #pragma unroll
@@ -243,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
     const int wq = warp & 3;                       // TMEM lane quarter
     const int row_in_tile = wq * 32 + lane;
     const int row = r0 + t * BM + row_in_tile;     // local row in chunk i
-    const int pos = p.q_start + row;               // absolute position
+    const int pos = q_start + row;               // absolute position
     const float sl2 = p.scale * kLog2e;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     const uint32_t sS = tS[t] + lane_off, sO = tO[t] + lane_off;
@@ -252,8 +268,8 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       // carry-in of an earlier window: natural-log m, l and the
       // unnormalised o_acc row go straight into O / the running state; the first
       // tile then proceeds like any later one (speculative exps + rescale check)
-      const bool ok = row < p.q_len;
-      const size_t vi = (size_t)head * p.q_len + row;
+      const bool ok = row < q_len;
+      const size_t vi = (size_t)head * q_len + row;
       const float m_in = ok ? p.m[vi] * kLog2e : -INFINITY;
       m_used = (m_in == -INFINITY) ? 0.f : m_in;
       l = ok ? p.l[vi] : 0.f;
@@ -385,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
     if (Tt > 0) {
       mbar_wait(&bars.o_full[t], (Tt - 1) & 1);
       tc_fence_after();
-      const bool ok = row < p.q_len;
+      const bool ok = row < q_len;
       if (!p.last) {
         // carry-out for the next window: unnormalised O, natural-log m, l
 #pragma unroll
@@ -402,8 +418,8 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
           }
         }
         if (ok) {
-          p.m[(size_t)head * p.q_len + row] = m_used * 0.6931471805599453f;
-          p.l[(size_t)head * p.q_len + row] = l;
+          p.m[(size_t)head * q_len + row] = m_used * 0.6931471805599453f;
+          p.l[(size_t)head * q_len + row] = l;
         }
       }
       if (p.last) {
@@ -432,14 +448,14 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
         fence_proxy_async_smem();
         named_bar_sync(9 + t, 128);  // the tile's four softmax warps staged their rows
         if (wq == 0 && lane == 0) {
-          const CUtensorMap* mo = tmap(a, a.o_slot);
+          const CUtensorMap* mo = tmap(a, o_slot);
           tma_store_3d(mo, qb, 0, head, r0 + t * BM);
           tma_store_3d(mo, qb + kHalf, 64, head, r0 + t * BM);
           bulk_commit();
           bulk_wait_read<0>();
         }
       }
-      if (ok && p.last) p.lse[(size_t)head * p.q_len + row] = (m_used + __log2f(l)) * 0.6931471805599453f;
+      if (ok && p.last) lse_out[(size_t)head * q_len + row] = (m_used + __log2f(l)) * 0.6931471805599453f;
     }
   }
   tc_fence_before();
@@ -453,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
 
 cudaError_t launch_fwd_sm100(const Sm100Fwd& a, cudaStream_t s) {
   if (a.p.d != HD) return cudaErrorNotSupported;
-  dim3 grid((a.p.q_len + 2 * BM - 1) / (2 * BM), a.p.heads);
+  dim3 grid(a.nq > 0 ? a.block_base[a.nq] : (a.p.q_len + 2 * BM - 1) / (2 * BM), a.p.heads);
   cudaError_t e = ensure_smem_attr((const void*)fwd_kernel, kSmemBytes);
   if (e != cudaSuccess) return e;
   fwd_kernel<<<grid, kThreads, kSmemBytes, s>>>(a);

@@ -96,7 +96,7 @@ struct DescKeyHash {
 // fit, the table is recycled BEFORE any slot of that call is resolved, after
 // every stream that launched from the table has drained (host wait; rare).
 constexpr int kDescSlots = 16384;          // kernels take uint16_t slot indices
-constexpr int kDescCallMax = 8 + 2 * kMaxWindow;
+constexpr int kDescCallMax = 8 + 4 * kMaxWindow;  // multi-chunk forward: K, V, Q, O of up to kMaxWindow chunks
 constexpr int kUploadEvents = 64;
 
 struct Coverage {
@@ -587,6 +587,82 @@ sppo_status sppo_attn_fwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
   if (e == cudaErrorNotSupported) return fail(SPPO_E_UNSUPPORTED, "this request is not implemented by the sm_100a kernels");
   if (e != cudaSuccess) return cuda_fail(e, "sppo_attn_fwd launch");
   commit_coverage(ctx->cov_fwd, q, chunk, kv, first, last);
+  return SPPO_OK;
+}
+
+// ---------------------------------------------------------------- forward of several chunks
+sppo_status sppo_attn_fwd_chunks(sppo_ctx ctx, const sppo_layout* L, int32_t i0, int32_t i1, const void* const* q,
+                                 const sppo_kv_set* kv, void* const* o, float* const* lse, void* stream) {
+  if (!ctx) return fail(SPPO_E_ARG, "ctx is NULL");
+  sppo_status s = check_layout(L, i0);
+  if (s) return s;
+  if (i1 <= i0 || i1 > L->num_chunks) return fail(SPPO_E_SHAPE, "chunk range [%d, %d) invalid", i0, i1);
+  if (i1 - i0 > kMaxWindow) return fail(SPPO_E_UNSUPPORTED, "more than %d chunks in one launch", kMaxWindow);
+  if (L->dtype != SPPO_BF16) return fail(SPPO_E_UNSUPPORTED, "multi-chunk forward: bf16 only");
+  if (!q || !o || !lse) return fail(SPPO_E_ARG, "q/o/lse arrays are NULL");
+  if (!kv || !kv->ids || !kv->k || !kv->v) return fail(SPPO_E_ARG, "kv set is NULL");
+  if (kv->n != i1) return fail(SPPO_E_ARG, "kv must hold exactly chunks 0..%d", i1 - 1);
+  for (int c = 0; c < kv->n; ++c) {
+    if (kv->ids[c] != c) return fail(SPPO_E_ARG, "kv ids must be 0..%d in ascending order", i1 - 1);
+    if (!kv->k[c] || !kv->v[c]) return fail(SPPO_E_ARG, "kv buffer %d is NULL", c);
+    if (!aligned16(kv->k[c]) || !aligned16(kv->v[c])) return fail(SPPO_E_ALIGN, "kv buffer %d not 16B aligned", c);
+  }
+  for (int k = 0; k < i1 - i0; ++k) {
+    if (!q[k] || !o[k] || !lse[k]) return fail(SPPO_E_ARG, "q/o/lse %d is NULL", k);
+    if (!aligned16(q[k]) || !aligned16(o[k]) || !aligned4(lse[k])) return fail(SPPO_E_ALIGN, "q/o/lse %d misaligned", k);
+  }
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  SPPO_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t strm = (cudaStream_t)stream;
+  Sm100Fwd a{};
+  FwdParams& p = a.p;
+  p.heads = L->heads;
+  p.d = L->head_dim;
+  p.scale = L->scale > 0.f ? L->scale : 1.f / sqrtf((float)L->head_dim);
+  p.first = 1;
+  p.last = 1;
+  p.q_start = (int32_t)L->offsets[i0];
+  p.q_len = (int32_t)(L->offsets[i0 + 1] - L->offsets[i0]);
+  p.trace = trace_for(ctx, i1 - 1, false);
+  a.n = kv->n;
+  a.nq = i1 - i0;
+  a.q0 = i0;
+  DescBlock db;
+  db.open(ctx);
+  std::vector<int> rk(kv->n), rv(kv->n), rq(a.nq), ro(a.nq);
+  for (int c = 0; c < kv->n; ++c) {
+    const int64_t len = L->offsets[c + 1] - L->offsets[c];
+    a.start[c] = (int32_t)L->offsets[c];
+    a.len[c] = (int32_t)len;
+    rk[c] = db.add(kv->k[c], len, p.heads, p.d, 128);
+    rv[c] = db.add(kv->v[c], len, p.heads, p.d, 128);
+  }
+  int blocks = 0;
+  for (int k = 0; k < a.nq; ++k) {
+    const int c = i1 - 1 - k;  // longest chunk first
+    const int64_t len = L->offsets[c + 1] - L->offsets[c];
+    rq[c - i0] = db.add(q[c - i0], len, p.heads, p.d, 128);
+    ro[c - i0] = db.add(o[c - i0], len, p.heads, p.d, 128);
+    a.lses[c - i0] = lse[c - i0];
+    a.block_base[k] = blocks;
+    blocks += (int)((len + 255) / 256);
+  }
+  a.block_base[a.nq] = blocks;
+  if ((s = db.resolve(strm))) return s;
+  for (int c = 0; c < kv->n; ++c) {
+    a.slots.k[c] = (uint16_t)db.slot(rk[c]);
+    a.slots.v[c] = (uint16_t)db.slot(rv[c]);
+  }
+  for (int k = 0; k < a.nq; ++k) {
+    a.qslots[k] = (uint16_t)db.slot(rq[k]);
+    a.oslots[k] = (uint16_t)db.slot(ro[k]);
+  }
+  a.q_slot = a.qslots[0];
+  a.o_slot = a.oslots[0];
+  a.desc_table = db.table();
+  cudaError_t e = launch_fwd_sm100(a, strm);
+  if (e == cudaErrorNotSupported) return fail(SPPO_E_UNSUPPORTED, "this request is not implemented by the sm_100a kernels");
+  if (e != cudaSuccess) return cuda_fail(e, "sppo_attn_fwd_chunks launch");
   return SPPO_OK;
 }
 

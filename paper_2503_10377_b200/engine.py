@@ -26,6 +26,7 @@ sized for the longest chunk and reused.
 from __future__ import annotations
 
 import functools
+import os
 import inspect
 
 import torch
@@ -75,6 +76,11 @@ class ChunkedAttention:
                 torch.tensor([], dtype=DTYPES[layout.dtype]).element_size()
             fwd_streams = 2 if (self._few_waves and kv_bytes <= 4e9) else 1
         self.fwd_streams = fwd_streams
+        # resident step(): all forward chunks in ONE launch (sppo_attn_fwd_chunks, bf16,
+        # single window per chunk), longest chunks first — no per-launch wave tails or
+        # launch gaps, and the CTAs of all chunks sweep the shared K/V together
+        self.fwd_multi = (layout.dtype == sppo.SPPO_BF16 and layout.num_chunks <= 256
+                          and os.environ.get("SPPO_FWD_MULTI", "1") != "0")
         self._side = None
         # instrumentation (tools/offload_timeline.py): when a list, every compute call
         # and every copy appends {kind, chunk, bytes, events}; see _tl_begin/_tl_end
@@ -214,6 +220,17 @@ class ChunkedAttention:
         strm = stream or torch.cuda.current_stream()
         self.dk_acc.zero_()
         self.dv_acc.zero_()
+        if self.fwd_multi and self.window >= N and not self.timing and self.timeline is None:
+            L = self.L
+            self.ctx.attn_fwd_chunks(L, 0, N, [self.rows(q, i) for i in range(N)], [self.rows(k, j) for j in range(N)],
+                                     [self.rows(v, j) for j in range(N)], [self.rows(self.o, i) for i in range(N)],
+                                     [self.lse_view(i) for i in range(N)], stream=strm)
+            self.launches += 1
+            if mark is not None:
+                mark.record(strm)
+            for i in range(N - 1, -1, -1):
+                self.backward_chunk(i, q, k, v, do, stream)
+            return dict(o=self.o, lse=self.lse, dq=self.dq, dk=self.dk, dv=self.dv)
         # two forward streams only without split windows (those share the carry scratch)
         two = self.fwd_streams > 1 and N > 1 and self.window >= N
         if two:

@@ -26,7 +26,7 @@ STATUS = {0: "SPPO_OK", 1: "SPPO_E_ARG", 2: "SPPO_E_SHAPE", 3: "SPPO_E_ALIGN", 4
 
 # every symbol include/sppo.h declares
 EXPORTS = ("sppo_ctx_create", "sppo_ctx_destroy", "sppo_ctx_sync", "sppo_last_error", "sppo_version",
-           "sppo_attn_fwd", "sppo_attn_bwd", "sppo_host_alloc", "sppo_host_free", "sppo_kv_offload",
+           "sppo_attn_fwd", "sppo_attn_fwd_chunks", "sppo_attn_bwd", "sppo_host_alloc", "sppo_host_free", "sppo_kv_offload",
            "sppo_kv_prefetch", "sppo_partition_equal", "sppo_partition_balanced", "sppo_partition_balanced_lin", "sppo_causal_pairs",
            "sppo_offload_alpha",
            "sppo_finalize", "sppo_ctx_streams", "sppo_ctx_numa_node")
@@ -85,6 +85,8 @@ def _load():
         "sppo_version": ([], i32),
         "sppo_attn_fwd": ([vp, C.POINTER(_Layout), i32, vp, C.POINTER(_KvSet), i32, C.POINTER(_FwdState), vp, vp, vp],
                           i32),
+        "sppo_attn_fwd_chunks": ([vp, C.POINTER(_Layout), i32, i32, C.POINTER(vp), C.POINTER(_KvSet), C.POINTER(vp),
+                                  C.POINTER(vp), vp], i32),
         "sppo_attn_bwd": ([vp, C.POINTER(_Layout), i32, vp, C.POINTER(_KvSet), C.POINTER(_BwdArgs), i32, vp], i32),
         "sppo_host_alloc": ([vp, sz, C.POINTER(vp)], i32),
         "sppo_host_free": ([vp, vp], i32),
@@ -281,6 +283,15 @@ class Context:
             st = _FwdState(_ptr(state[0]), _ptr(state[1]), _ptr(state[2]))
         _check(_lib.sppo_attn_fwd(self.h, C.byref(layout.c), chunk, _ptr(q), C.byref(kv), flags,
                                   C.byref(st) if st is not None else None, _ptr(o), _ptr(lse), _stream(stream)))
+
+    def attn_fwd_chunks(self, layout: Layout, i0: int, i1: int, qs, ks, vs, os_, lses, stream=None):
+        """sppo_attn_fwd_chunks: chunks i0..i1-1 in one launch (ks, vs: chunks 0..i1-1)."""
+        n = i1 - i0
+        kv = _kvset(list(range(len(ks))), ks, vs)  # the C side checks they are exactly 0..i1-1
+        _check(_lib.sppo_attn_fwd_chunks(self.h, C.byref(layout.c), i0, i1,
+                                         (C.c_void_p * n)(*[_ptr(t) for t in qs]), C.byref(kv),
+                                         (C.c_void_p * n)(*[_ptr(t) for t in os_]),
+                                         (C.c_void_p * n)(*[_ptr(t) for t in lses]), _stream(stream)))
 
     def attn_bwd(self, layout: Layout, chunk: int, q, kv_ids, ks, vs, o, lse, dout, delta, dq_acc, dk_accs,
                  dv_accs, dq=None, dk=None, dv=None, flags=SPPO_FIRST | SPPO_LAST, stream=None):

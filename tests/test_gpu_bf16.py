@@ -178,3 +178,63 @@ def test_bf16_custom_scale_and_growing_max(ctx, scale, window):
     for key in ("dq", "dk", "dv"):
         got = getattr(eng, key).double().cpu().numpy()
         np.testing.assert_allclose(got, ref[key], atol=g_atol, rtol=5e-2, err_msg=key)
+
+
+@pytest.mark.parametrize("S,h,offsets,i0,i1", [(3000, 2, None, 0, 6), (2300, 3, [0, 5, 300, 301, 1024, 1500, 2300], 2, 6),
+                                               (1100, 1, None, 3, 4)])
+def test_multi_chunk_forward_matches_oracle_and_per_chunk(ctx, S, h, offsets, i0, i1):
+    """sppo_attn_fwd_chunks (chunks i0..i1-1 in one launch, longest first) against
+    the oracle, and BITWISE equal to per-chunk sppo_attn_fwd (same tiles, same
+    per-row arithmetic: the launch only changes which CTA does which tile)."""
+    from paper_2503_10377_b200 import sppo
+    off = offsets or ragged_offsets(S, 6, seed=S)
+    x, dev = make(S, h, seed=S + i0)
+    L = sppo.Layout(h, 128, off)
+    rows = lambda t, i: t[off[i]:off[i + 1]]  # noqa: E731
+    lse_v = lambda t, i: t[off[i] * h:off[i + 1] * h]  # noqa: E731
+    o1, o2 = torch.zeros_like(dev["q"]), torch.zeros_like(dev["q"])
+    l1 = torch.zeros(S * h, dtype=torch.float32, device="cuda")
+    l2 = torch.zeros_like(l1)
+    ctx.attn_fwd_chunks(L, i0, i1, [rows(dev["q"], i) for i in range(i0, i1)], [rows(dev["k"], j) for j in range(i1)],
+                        [rows(dev["v"], j) for j in range(i1)], [rows(o1, i) for i in range(i0, i1)],
+                        [lse_v(l1, i) for i in range(i0, i1)])
+    for i in range(i0, i1):
+        ctx.attn_fwd(L, i, rows(dev["q"], i), list(range(i + 1)), [rows(dev["k"], j) for j in range(i + 1)],
+                     [rows(dev["v"], j) for j in range(i + 1)], o=rows(o2, i), lse=lse_v(l2, i))
+    torch.cuda.synchronize()
+    ctx.sync()
+    a, b = off[i0], off[i1]
+    assert torch.equal(o1[a:b], o2[a:b]) and torch.equal(l1[a * h:b * h], l2[a * h:b * h])
+    assert not o1[:a].any() and not o1[b:].any()  # nothing outside the chunk range written
+    xn = {k: v.double().numpy() for k, v in x.items()}
+    o_ref, lse_ref = oracle.causal_attention_dense(xn["q"], xn["k"], xn["v"])
+    np.testing.assert_allclose(o1[a:b].double().cpu().numpy(), o_ref[a:b], **O_TOL)
+    lse = l1.view(-1)
+    got = np.concatenate([lse_v(lse, i).view(h, -1).double().cpu().numpy() for i in range(i0, i1)], axis=1)
+    np.testing.assert_allclose(got, lse_ref[:, a:b], **LSE_TOL)
+
+
+def test_multi_chunk_forward_argument_errors(ctx):
+    from paper_2503_10377_b200 import sppo
+    S, h = 512, 1
+    off = [0, 128, 256, 512]
+    x, dev = make(S, h, seed=5)
+    L = sppo.Layout(h, 128, off)
+    o = torch.empty_like(dev["q"])
+    lse = torch.empty(S * h, dtype=torch.float32, device="cuda")
+    rows = lambda t, i: t[off[i]:off[i + 1]]  # noqa: E731
+    with pytest.raises(sppo.SppoError) as e:  # kv must be exactly 0..i1-1
+        ctx.attn_fwd_chunks(L, 0, 2, [rows(dev["q"], i) for i in range(2)], [rows(dev["k"], j) for j in range(3)],
+                            [rows(dev["v"], j) for j in range(3)], [rows(o, i) for i in range(2)],
+                            [lse[off[i] * h:off[i + 1] * h] for i in range(2)])
+    assert e.value.name == "SPPO_E_ARG"
+    with pytest.raises(sppo.SppoError) as e:  # empty range
+        ctx.attn_fwd_chunks(L, 2, 2, [], [rows(dev["k"], j) for j in range(2)], [rows(dev["v"], j) for j in range(2)],
+                            [], [])
+    assert e.value.name == "SPPO_E_SHAPE"
+    Lf = sppo.Layout(h, 128, off, dtype=sppo.SPPO_FP32)
+    xf = {k: v.float() for k, v in dev.items()}
+    with pytest.raises(sppo.SppoError) as e:  # fp32: per-chunk calls only
+        ctx.attn_fwd_chunks(Lf, 0, 1, [rows(xf["q"], 0)], [rows(xf["k"], 0)], [rows(xf["v"], 0)],
+                            [rows(xf["q"], 0)], [lse[:128]])
+    assert e.value.name == "SPPO_E_UNSUPPORTED"
