@@ -96,6 +96,11 @@ constexpr uint32_t kOffDelta = kOffLSE + 1024;    // 2 x 128 fp32
 // ~40 % of the kernel's LSU shared-memory wavefronts).  No-swizzle K-major core
 // matrices: element (row, k) at (row/8)*256 + (k/8)*128 + (row%8)*16 + (k%8)*2.
 constexpr bool kFold = SPPO_BWD_FOLD;
+#ifndef SPPO_WARP_ARRIVE
+#define SPPO_WARP_ARRIVE 1  // consumer releases (LSE / Delta / dS-local) as one arrival per warp after __syncwarp
+#endif
+constexpr bool kWarpArrive = SPPO_WARP_ARRIVE;
+constexpr uint32_t kComputeArrivals = kWarpArrive ? 8 : 256;  // 8 compute warps x (1 or 32 lanes)
 constexpr uint32_t kOffXK = kOffDelta + 1024;   // [128 keys][16]: ones at k = 0, 1 (A of the extra step)
 constexpr uint32_t kOffXQ = kOffXK + 4096;      // [64 q][16]: -LSE/tau hi, lo (B of S^T's extra step)
 constexpr uint32_t kOffXO = kOffXQ + 2048;      // [64 q][16]: -Delta hi, lo (B of dP^T's extra step)
@@ -189,15 +194,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&bars.oa_empty[s], 1);
       mbar_init(&bars.lse_full[s], 32);
       mbar_init(&bars.delta_full[s], 32);
-      mbar_init(&bars.lse_empty[s], 256);
-      mbar_init(&bars.delta_empty[s], 256);
+      mbar_init(&bars.lse_empty[s], kComputeArrivals);
+      mbar_init(&bars.delta_empty[s], kComputeArrivals);
     }
     mbar_init(&bars.s_full, 1);
     mbar_init(&bars.dp_full, 1);
     mbar_init(&bars.dq_full, 1);
     mbar_init(&bars.p_full, 16);
     mbar_init(&bars.ds_full, 16);
-    mbar_init(&bars.ds_local, 256);
+    mbar_init(&bars.ds_local, kComputeArrivals);
     mbar_init(&bars.dq_free, 8);
     mbar_init(&bars.dkdv_done, 1);
     fence_mbar_init();
@@ -583,9 +588,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       tmem_wait_st();
       tc_fence_before();
-      if (!kFold) mbar_arrive(&bars.lse_empty[s]);  // every thread: its LSE reads are done
+      if (!kFold && !kWarpArrive) mbar_arrive(&bars.lse_empty[s]);  // every thread: its LSE reads are done
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(L_p_full);
+      if (lane == 0) {
+        if (!kFold && kWarpArrive) mbar_arrive(&bars.lse_empty[s]);  // the warp's LSE reads are done
+        mbar_arrive_cluster(L_p_full);
+      }
       if (lane == 0 && wq == 0 && g == 0) TR(7, m);
 
       // ---- dS = P (dP - Delta)   (tau is applied to dK / dQ at their write-out)
@@ -628,10 +636,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
       fence_proxy_async_smem();
       tc_fence_before();
-      if (!kFold) mbar_arrive(&bars.delta_empty[s]);  // every thread: its Delta reads are done
-      if (!leader) mbar_arrive(&bars.ds_local);  // the peer's own dQ MMA waits on this
+      if (!kWarpArrive) {
+        if (!kFold) mbar_arrive(&bars.delta_empty[s]);  // every thread: its Delta reads are done
+        if (!leader) mbar_arrive(&bars.ds_local);  // the peer's own dQ MMA waits on this
+      }
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(L_ds_full);
+      if (lane == 0) {
+        if (kWarpArrive) {
+          if (!kFold) mbar_arrive(&bars.delta_empty[s]);  // the warp's Delta reads are done
+          if (!leader) mbar_arrive(&bars.ds_local);  // its dS stores fenced: the peer's own dQ MMA waits on this
+        }
+        mbar_arrive_cluster(L_ds_full);
+      }
 #ifdef SPPO_TRACE_DS
       if (lane == 0 && wq == 0 && g == 0) TR(9, m);
 #else

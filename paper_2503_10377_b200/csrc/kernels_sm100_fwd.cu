@@ -40,6 +40,10 @@ constexpr float kRescaleThreshold = 8.0f;        // log2 units
 #define SPPO_EMU_EVERY 4  // measured best among 2, 3, 4, 6 (tools/gpu_abn.sh)
 #endif
 constexpr int kEmuEvery = SPPO_EMU_EVERY;        // 1 of every kEmuEvery exp2 pairs on the FMA pipe
+#ifndef SPPO_WARP_ARRIVE
+#define SPPO_WARP_ARRIVE 1  // P-ready signals as one arrival per warp after __syncwarp
+#endif
+constexpr bool kWarpArrive = SPPO_WARP_ARRIVE;
 
 constexpr uint32_t kIdescS = idesc_bf16(128, 128, 0, 0);   // Q (K-major) x K (K-major)
 constexpr uint32_t kIdescPV = idesc_bf16(128, 128, 0, 1);  // P (TMEM) x V (MN-major)
@@ -136,8 +140,8 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       mbar_init(&bars.v_full[s], 1);
       mbar_init(&bars.v_empty[s], 1);
       mbar_init(&bars.s_full[s], 1);
-      mbar_init(&bars.p_full[s][0], 128);
-      mbar_init(&bars.p_full[s][1], 128);
+      mbar_init(&bars.p_full[s][0], kWarpArrive ? 4 : 128);
+      mbar_init(&bars.p_full[s][1], kWarpArrive ? 4 : 128);
       mbar_init(&bars.o_full[s], 1);
     }
     fence_mbar_init();
@@ -389,13 +393,23 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       tmem_st32(sS + 0, pk0);  // P keys 0..63 -> the MMA warp starts PV's first half
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&bars.p_full[t][0]);
+      if (kWarpArrive) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.p_full[t][0]);
+      } else {
+        mbar_arrive(&bars.p_full[t][0]);
+      }
       exps(64, -m_used, &r[32], ls1);  // keys 64..127 packed over r[32..63] (already consumed)
       tmem_st32(sS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
       tmem_wait_st();
       tc_fence_before();
       if (lane == 0 && wq == 0) TR(7 + 3 * t, n);
-      mbar_arrive(&bars.p_full[t][1]);
+      if (kWarpArrive) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.p_full[t][1]);
+      } else {
+        mbar_arrive(&bars.p_full[t][1]);
+      }
       l += ls0.x + ls0.y + ls1.x + ls1.y;
     }
     if (Tt > 0) {
