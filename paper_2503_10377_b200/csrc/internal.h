@@ -54,11 +54,17 @@ struct BwdParams {
   void* dk_out;
   void* dv_out;
   unsigned long long* trace;  // debug: per-event clock64 stamps of CTA (0, 0), or null
+  int32_t trace_life;         // debug: trace holds kLifeSlots stamps per CTA of the launch instead
 };
 
 // Debug tracing (env SPPO_TRACE=<file>): slot layout trace[iter * kTraceSlots + event]
 constexpr int kTraceSlots = 16;
 constexpr int kTraceIters = 512;
+// Lifetime mode (env SPPO_TRACE_LIFE=1, bwd only): trace[cta * kLifeSlots + k], cta =
+// blockIdx.y * gridDim.x + blockIdx.x; stamps (clock64): 0 entry, 1 setup done,
+// 2 first S seen, 3 loop done, 4 dK/dV done seen, 5 epilogue issued, 6 exit, 7 smid | M << 32
+constexpr int kLifeSlots = 8;
+constexpr size_t kLifeWords = (size_t)1 << 22;
 
 // ---- SIMT kernels (fp32 path; exact FP32 FMA, no tensor cores) ----------
 cudaError_t launch_fwd_simt_f32(const FwdParams& p, const KvWindow& w, cudaStream_t s);
@@ -102,6 +108,8 @@ struct Sm100Bwd {
   int32_t len[kMaxWindow];
   int32_t pair_base[kMaxWindow + 1];  // prefix count of 256-key CTA-pair tiles per window chunk
   TmaSlots slots;
+  TmaSlots acc;  // fp32 dK (acc.k) / dV (acc.v) accumulator maps (TMA reduce-add of the item epilogue)
+  int* sched;    // item counter of this launch (zeroed on the stream before it): dynamic item schedule
   float* dk[kMaxWindow];
   float* dv[kMaxWindow];
 };

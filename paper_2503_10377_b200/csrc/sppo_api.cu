@@ -95,6 +95,7 @@ struct DescKeyHash {
 // offload / prefetch copies on the copy engines.  When a call's new maps do not
 // fit, the table is recycled BEFORE any slot of that call is resolved, after
 // every stream that launched from the table has drained (host wait; rare).
+constexpr int kSchedSlots = 1024;          // persistent-bwd item counters (one per launch in flight)
 constexpr int kDescSlots = 16384;          // kernels take uint16_t slot indices
 constexpr int kDescCallMax = 8 + 4 * kMaxWindow;  // multi-chunk forward: K, V, Q, O of up to kMaxWindow chunks
 constexpr int kUploadEvents = 64;
@@ -113,6 +114,10 @@ struct sppo_ctx_s {
   // TMA descriptors: persistent device table + pinned host mirror, key -> slot,
   // per-slot upload record (event id, its generation, upload stream, observed done)
   CUtensorMap* desc_dev = nullptr;
+  // persistent bwd item counters: one int per launch, taken round-robin and zeroed on
+  // the launch stream just before the kernel (kSchedSlots launches may be in flight)
+  int* sched = nullptr;
+  unsigned sched_next = 0;
   CUtensorMap* desc_host = nullptr;
   std::unordered_map<DescKey, int, DescKeyHash> desc_slot;
   struct SlotUpload {
@@ -139,6 +144,7 @@ struct sppo_ctx_s {
   unsigned long long* trace = nullptr;
   int trace_chunk = -1;
   int trace_bwd = 1;
+  int trace_life = 0;  // SPPO_TRACE_LIFE: per-CTA lifetime stamps of the traced bwd launch
 };
 
 namespace {
@@ -152,6 +158,21 @@ unsigned long long* trace_for(sppo_ctx ctx, int chunk, bool bwd) {
 void trace_dump(sppo_ctx ctx) {
   const char* path = getenv("SPPO_TRACE");
   if (!ctx->trace || !path) return;
+  if (ctx->trace_life) {
+    std::vector<unsigned long long> h(sppo::kLifeWords);
+    if (cudaMemcpy(h.data(), ctx->trace, sppo::kLifeWords * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    FILE* f = fopen(path, "w");
+    if (!f) return;
+    for (size_t c = 0; c < sppo::kLifeWords / sppo::kLifeSlots; ++c) {
+      const unsigned long long* r = &h[c * sppo::kLifeSlots];
+      if (r[0] == 0) continue;
+      fprintf(f, "%zu", c);
+      for (int s = 0; s < sppo::kLifeSlots; ++s) fprintf(f, " %llu", r[s]);
+      fprintf(f, "\n");
+    }
+    fclose(f);
+    return;
+  }
   std::vector<unsigned long long> h(kTraceWords);
   if (cudaMemcpy(h.data(), ctx->trace, kTraceWords * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
   FILE* f = fopen(path, "w");
@@ -444,6 +465,7 @@ sppo_status sppo_ctx_create(int device, sppo_ctx* out) {
       (e = cudaEventCreateWithFlags(&c->ev_cons, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaMalloc(&c->desc_dev, sizeof(CUtensorMap) * kDescSlots)) != cudaSuccess ||
+      (e = cudaMalloc(&c->sched, sizeof(int) * kSchedSlots)) != cudaSuccess ||
       (e = cudaHostAlloc(&c->desc_host, sizeof(CUtensorMap) * kDescSlots, cudaHostAllocDefault)) !=
           cudaSuccess) {
     sppo_ctx_destroy(c);
@@ -461,8 +483,9 @@ sppo_status sppo_ctx_create(int device, sppo_ctx* out) {
     const char* kind = getenv("SPPO_TRACE_KIND");
     c->trace_chunk = ch ? atoi(ch) : 0;
     c->trace_bwd = (kind && strcmp(kind, "fwd") == 0) ? 0 : 1;
-    if (cudaMalloc(&c->trace, kTraceWords * 8) != cudaSuccess ||
-        cudaMemset(c->trace, 0, kTraceWords * 8) != cudaSuccess)
+    c->trace_life = getenv("SPPO_TRACE_LIFE") && c->trace_bwd ? 1 : 0;
+    const size_t words = c->trace_life ? sppo::kLifeWords : kTraceWords;
+    if (cudaMalloc(&c->trace, words * 8) != cudaSuccess || cudaMemset(c->trace, 0, words * 8) != cudaSuccess)
       c->trace = nullptr;
   }
   *out = c;
@@ -489,6 +512,7 @@ sppo_status sppo_ctx_destroy(sppo_ctx c) {
   for (int b = 0; b < kUploadEvents; ++b)
     if (c->up_ev[b]) cudaEventDestroy(c->up_ev[b]);
   if (c->desc_dev) cudaFree(c->desc_dev);
+  if (c->sched) cudaFree(c->sched);
   if (c->desc_host) cudaFreeHost(c->desc_host);
   if (c->trace) cudaFree(c->trace);
   delete c;
@@ -716,6 +740,7 @@ sppo_status sppo_attn_bwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
   p.dk_out = a->dk;
   p.dv_out = a->dv;
   p.trace = trace_for(ctx, chunk, true);
+  p.trace_life = ctx->trace_life;
   const bool bf16 = L->dtype == SPPO_BF16;
   cudaError_t e = cudaSuccess;
   // host-side preparation first (nothing is enqueued if it fails), then
@@ -742,11 +767,13 @@ sppo_status sppo_attn_bwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
     const int rq64 = db.add(q, p.q_len, p.heads, p.d, 64);
     const int rdo64 = db.add(a->dout, p.q_len, p.heads, p.d, 64);
     const int rdq = db.add(a->dq_acc, p.q_len, p.heads, p.d, 128, 4);
-    std::vector<int> rk(kv->n), rv(kv->n);
+    std::vector<int> rk(kv->n), rv(kv->n), rdk(kv->n), rdv(kv->n);
     int pairs = 0;
     for (int c = 0; c < kv->n; ++c) {
       rk[c] = db.add(kv->k[c], w.len[c], p.heads, p.d, 128);
       rv[c] = db.add(kv->v[c], w.len[c], p.heads, p.d, 128);
+      rdk[c] = db.add(a->dk_acc[c], w.len[c], p.heads, p.d, 128, 4);
+      rdv[c] = db.add(a->dv_acc[c], w.len[c], p.heads, p.d, 128, 4);
       sa.start[c] = w.start[c];
       sa.len[c] = w.len[c];
       sa.pair_base[c] = pairs;
@@ -764,9 +791,13 @@ sppo_status sppo_attn_bwd(sppo_ctx ctx, const sppo_layout* L, int32_t chunk, con
     for (int c = 0; c < kv->n; ++c) {
       sa.slots.k[c] = (uint16_t)db.slot(rk[c]);
       sa.slots.v[c] = (uint16_t)db.slot(rv[c]);
+      sa.acc.k[c] = (uint16_t)db.slot(rdk[c]);
+      sa.acc.v[c] = (uint16_t)db.slot(rdv[c]);
     }
     sa.desc_table = db.table();
+    sa.sched = ctx->sched + (ctx->sched_next++ % kSchedSlots);
     if ((e = preprocess()) != cudaSuccess) return cuda_fail(e, "bwd preprocess");
+    if ((e = cudaMemsetAsync(sa.sched, 0, sizeof(int), strm)) != cudaSuccess) return cuda_fail(e, "bwd scheduler reset");
     e = launch_bwd_sm100(sa, strm);
   }
   if (e == cudaErrorNotSupported) return fail(SPPO_E_UNSUPPORTED, "this request is not implemented by the sm_100a kernels");
