@@ -100,6 +100,12 @@ constexpr uint32_t kIdescT = idesc_bf16(256, 128, 0, 1);  // pair, TMEM or K-maj
 constexpr uint32_t kIdescQ = idesc_bf16(128, 128, 1, 1);  // one CTA, MN-major x MN-major
 constexpr float kLog2e = 1.4426950408889634f;
 
+#ifndef SPPO_BWD_KV_LANES
+#define SPPO_BWD_KV_LANES 1  // K / V loads issued by lanes 1 / 2 of warp 13, Q rows by lane 0: bwd +1.9 % (1094 vs 1075 TF/s)
+#endif
+constexpr int kKLane = SPPO_BWD_KV_LANES ? 1 : 0, kVLane = SPPO_BWD_KV_LANES ? 2 : 0;
+// (Measured without gain: the Q column half issued by a second lane of warp 14, and
+// each staging buffer's reduces issued by its own reducer warp: bwd within +-0.5 %.)
 // Item ring depth: the scheduler runs at most ~4 items ahead of the slowest consumer
 // (the reducers): publishing item j+4 (during item j+3) needs item j+3's K loaded ->
 // k_free(j+2) -> the MMA finished item j+2 -> acc_free(j+1) -> the reducers read
@@ -276,7 +282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // K of the pair's j-th item, once item j-1's MMAs have read the buffer
       auto load_k = [&](int j, const Item& I) {
         if (j >= 1) mbar_wait(&bars.k_free, (j - 1) & 1);
-        if (lane == 0) {
+        if (lane == kKLane) {
           const CUtensorMap* mk = tmap(a, a.slots.k[I.c]);
           if (leader) mbar_arrive_expect_tx(&bars.k_full, 2 * kTile);
           tma_load_3d_pair(smem + kOffK, mk, L_k, 0, I.head, I.kv_row0);
@@ -304,7 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           if (m == 0) {  // this item's V once the previous item's last dP^T has read the buffer
             if (j > 0) mbar_wait(&bars.v_free, (j - 1) & 1);
-            if (lane == 0) {
+            if (lane == kVLane) {
               const CUtensorMap* mv = tmap(a, a.slots.v[I.c]);
               if (leader) mbar_arrive_expect_tx(&bars.v_full, 2 * kTile);
               tma_load_3d_pair(smem + kOffV, mv, L_v, 0, I.head, I.kv_row0);
@@ -448,6 +454,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (k >= n_items) break;
           const int M = get_item(a, k, rank).M;
           mbar_wait(&bars.k_full, j & 1);  // this item's K (both CTAs)
+          if (gt > 0) TR(3, gt - 1);       // (trace: slot 3 of an item's last tile = next K arrived)
           issue_s(gt);  // S^T of the item's first tile: P of the previous tile consumed (in-order pipe)
           for (int m = 0; m < M; ++m, ++gt) {
             TR(0, gt);
