@@ -173,7 +173,10 @@ typedef struct {
  *   Delta_p = <dO_p, O_p>;  P = exp(tau q.k - LSE);  dV_j += P^T dO_i;
  *   dP = dO_i V_j^T;  dS = P (dP - Delta);  dQ_i += tau dS K_j;
  *   dK_j += tau dS^T Q_i   for every j in the window.
- * Enqueued on `stream`.
+ * Enqueued on `stream`: Delta (FIRST), a 4-byte reset of the launch's work counter,
+ * the backward kernel (bf16: persistent CTA pairs taking 256-key x head items from
+ * that counter), the dQ cast (LAST).  dK_j/dV_j accumulate by TMA reduce-add, so
+ * the order of the fp32 additions into dk_acc/dv_acc is not fixed.
  */
 sppo_status sppo_attn_bwd(sppo_ctx ctx, const sppo_layout* layout, int32_t chunk,
                           const void* q, const sppo_kv_set* kv, const sppo_bwd_args* a,

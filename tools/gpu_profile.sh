@@ -13,7 +13,7 @@ fi
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2_$tag.csv \
   python bench.py --steps 1 --warmup 0 --no-e2e --no-offload --no-cpu > /dev/null 2>&1
 for k in bwd fwd; do
-  skip=15; [ $k = bwd ] && skip=0   # chunk 15 = first bwd launch (N-1 .. 0), last fwd launch
+  skip=0   # bwd: chunk 15 = first launch (N-1 .. 0); fwd: the one multi-chunk launch of the step
   SPPO_TRACE_KIND=$k timeout 900 ncu --set full --clock-control none --import-source on -k regex:${k}_kernel \
     --launch-skip $skip -c 1 -f -o gpurun_out/prof_${k}_$tag python tools/trace_run.py > /dev/null 2>&1
   ncu -i gpurun_out/prof_${k}_$tag.ncu-rep --page details --csv > gpurun_out/prof_${k}_${tag}_details.csv 2>/dev/null
