@@ -50,6 +50,7 @@ def _on_step_stream(fn):
     return run
 
 DTYPES = {sppo.SPPO_BF16: torch.bfloat16, sppo.SPPO_FP32: torch.float32}
+DTYPE_BYTES = {sppo.SPPO_BF16: 2, sppo.SPPO_FP32: 4}
 
 
 class ChunkedAttention:
@@ -79,7 +80,13 @@ class ChunkedAttention:
         # resident step(): all forward chunks in ONE launch (sppo_attn_fwd_chunks, bf16,
         # single window per chunk), longest chunks first — no per-launch wave tails or
         # launch gaps, and the CTAs of all chunks sweep the shared K/V together
-        self.fwd_multi = (layout.dtype == sppo.SPPO_BF16 and layout.num_chunks <= 256
+        # — while one head's K/V sweep stays moderate: the CTAs of different chunks start
+        # at different times, so with several GB per head they stream it out of step,
+        # where each per-chunk launch keeps its CTAs together (C5 per-GPU share, 2 GB of
+        # K/V per head: forward 977.6 one launch vs 1000.1 per chunk; C3, 0.5 GB per
+        # head: 1126.7 one launch)
+        kv_head = layout.offsets[-1] * layout.head_dim * 2 * DTYPE_BYTES.get(layout.dtype, 4)
+        self.fwd_multi = (layout.dtype == sppo.SPPO_BF16 and layout.num_chunks <= 256 and kv_head <= 1 << 30
                           and os.environ.get("SPPO_FWD_MULTI", "1") != "0")
         self._side = None
         # instrumentation (tools/offload_timeline.py): when a list, every compute call
