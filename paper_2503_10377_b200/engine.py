@@ -55,7 +55,7 @@ DTYPE_BYTES = {sppo.SPPO_BF16: 2, sppo.SPPO_FP32: 4}
 
 class ChunkedAttention:
     def __init__(self, ctx: sppo.Context, layout: sppo.Layout, device="cuda", window: int | None = None,
-                 timing: bool = False, fwd_streams: int | None = None):
+                 timing: bool = False, fwd_streams: int | None = None, fwd_group: int | None = None):
         self.ctx, self.L = ctx, layout
         # resident step(): forward chunks are independent (chunk i reads only inputs), so
         # consecutive forward launches may alternate between two streams and the next one
@@ -80,14 +80,19 @@ class ChunkedAttention:
         # resident step(): all forward chunks in ONE launch (sppo_attn_fwd_chunks, bf16,
         # single window per chunk), longest chunks first — no per-launch wave tails or
         # launch gaps, and the CTAs of all chunks sweep the shared K/V together
-        # — while one head's K/V sweep stays moderate: the CTAs of different chunks start
-        # at different times, so with several GB per head they stream it out of step,
-        # where each per-chunk launch keeps its CTAs together (C5 per-GPU share, 2 GB of
-        # K/V per head: forward 977.6 one launch vs 1000.1 per chunk; C3, 0.5 GB per
-        # head: 1126.7 one launch)
+        # — while one head's K/V sweep stays moderate.  The CTAs of different chunks start
+        # at different times, so with several GB per head they stream it out of step
+        # (C5 per-GPU share, 2 GB of K/V per head: forward 977.6 in one launch vs 1000.1
+        # per chunk; C3, 0.5 GB per head: 1126.7 in one launch); there the launches take
+        # groups of consecutive chunks (nearly the same key range) of >= 8 waves, so a
+        # group's CTAs stay together and the per-chunk launches' last-wave tails go
+        # (C5 share: a 16K chunk is 512 CTAs = 3.5 waves)
         kv_head = layout.offsets[-1] * layout.head_dim * 2 * DTYPE_BYTES.get(layout.dtype, 4)
-        self.fwd_multi = (layout.dtype == sppo.SPPO_BF16 and layout.num_chunks <= 256 and kv_head <= 1 << 30
+        self.fwd_multi = (layout.dtype == sppo.SPPO_BF16 and layout.num_chunks <= 256
                           and os.environ.get("SPPO_FWD_MULTI", "1") != "0")
+        if fwd_group is None:
+            fwd_group = layout.num_chunks if kv_head <= 1 << 30 else -(-8 * sms // max(1, ctas))
+        self.fwd_group = max(1, min(fwd_group, layout.num_chunks))
         self._side = None
         # instrumentation (tools/offload_timeline.py): when a list, every compute call
         # and every copy appends {kind, chunk, bytes, events}; see _tl_begin/_tl_end
@@ -228,11 +233,14 @@ class ChunkedAttention:
         self.dk_acc.zero_()
         self.dv_acc.zero_()
         if self.fwd_multi and self.window >= N and not self.timing and self.timeline is None:
-            L = self.L
-            self.ctx.attn_fwd_chunks(L, 0, N, [self.rows(q, i) for i in range(N)], [self.rows(k, j) for j in range(N)],
-                                     [self.rows(v, j) for j in range(N)], [self.rows(self.o, i) for i in range(N)],
-                                     [self.lse_view(i) for i in range(N)], stream=strm)
-            self.launches += 1
+            L, G = self.L, self.fwd_group
+            ks, vs = [self.rows(k, j) for j in range(N)], [self.rows(v, j) for j in range(N)]
+            for i0 in range(0, N, G):
+                i1 = min(N, i0 + G)
+                self.ctx.attn_fwd_chunks(L, i0, i1, [self.rows(q, i) for i in range(i0, i1)], ks[:i1], vs[:i1],
+                                         [self.rows(self.o, i) for i in range(i0, i1)],
+                                         [self.lse_view(i) for i in range(i0, i1)], stream=strm)
+                self.launches += 1
             if mark is not None:
                 mark.record(strm)
             for i in range(N - 1, -1, -1):

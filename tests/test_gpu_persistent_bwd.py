@@ -79,3 +79,25 @@ def test_rerun_is_stable(ctx):
     e2 = run(ctx, S, h, off, seed=23)
     d = (e2.dk.float() - dk1).abs().max().item()
     assert d <= 2e-2 * max(1.0, dk1.abs().max().item())
+
+
+@pytest.mark.parametrize("group", [1, 2, 3])
+def test_grouped_multichunk_forward(ctx, group):
+    # the resident step's forward as launches over groups of consecutive chunks (the
+    # long-sequence schedule) equals the oracle; group 1 = per-chunk
+    # multi-launch form, group 3 leaves a ragged last group
+    from paper_2503_10377_b200 import engine, sppo
+    S, h = 1500, 6
+    off = [0, 200, 512, 700, 1024, 1300, 1500]
+    x = make_inputs(S, range(h), 128, seed=30 + group, dtype=torch.bfloat16)
+    dev = {k: v.cuda() for k, v in x.items()}
+    eng = engine.ChunkedAttention(ctx, sppo.Layout(h, 128, off, dtype=sppo.SPPO_BF16), fwd_group=group)
+    assert eng.fwd_multi and eng.fwd_group == group
+    eng.step(dev["q"], dev["k"], dev["v"], dev["do"])
+    torch.cuda.synchronize()
+    ctx.sync()
+    xn = {k: v.double().numpy() for k, v in x.items()}
+    ref = oracle.causal_attention_dense_bwd(xn["q"], xn["k"], xn["v"], xn["do"])
+    np.testing.assert_allclose(eng.o.double().cpu().numpy(), ref["o"], **O_TOL)
+    for key in ("dq", "dk", "dv"):
+        np.testing.assert_allclose(getattr(eng, key).double().cpu().numpy(), ref[key], **G_TOL, err_msg=key)
