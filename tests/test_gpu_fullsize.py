@@ -106,7 +106,8 @@ def test_c2_early_key_grads_accumulated_over_all_chunks():
 
 
 def test_c3_last_keys_grads():
-    """C3 on one GPU (resident, one launch per chunk as the bench times it):
+    """C3 on one GPU (resident step as the bench times it: the forward in one
+    multi-chunk launch, one persistent backward launch per chunk):
     sampled keys of the last 4096 positions (chunk 63, contributions of chunk 63
     only plus the diagonal), rows at every 16th boundary, identities."""
     from paper_2503_10377_b200 import engine, sppo
