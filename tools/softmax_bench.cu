@@ -3,7 +3,8 @@
 // thread, row max, 128 exponentials (1 of every EMU pairs through the FMA-pipe
 // cubic), row sum, bf16 pack, tcgen05.st of P.  Cycles per 128-element row per
 // warp with 1 or 2 such warps per SMSP — i.e. how long a tile's softmax takes
-// alone and how two tiles' softmax share an SMSP.
+// alone and how two tiles' softmax share an SMSP; optionally with a spare warp
+// streaming M=128 N=128 SS MMAs into other TMEM columns (the tensor core busy).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2503_10377_b200/csrc -o tools/softmax_bench tools/softmax_bench.cu
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -38,13 +39,38 @@ __device__ __forceinline__ void exps64(const float* s, int j0, float negm, float
 }
 
 template <int EMU, int SUMS>
-__global__ void __launch_bounds__(256, 1) softmax_kernel(int iters, long long* cyc, float* sink) {
+__global__ void __launch_bounds__(288, 1) softmax_kernel(int iters, long long* cyc, float* sink, int nsoft, int mma) {
   __shared__ uint32_t tmem_base;
+  __shared__ uint64_t mbar;
+  __shared__ volatile int done;
+  extern __shared__ __align__(1024) uint8_t dsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    fence_mbar_init();
+    done = 0;
+  }
+  if (warp == 0) tmem_alloc<512>(&tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (warp == nsoft) {  // MMA warp: S-like MMAs into columns 256..383 until the softmax warps finish
+    if (mma) {
+      const uint64_t da = sdesc_kmajor(smem_u32(dsm)), db = sdesc_kmajor(smem_u32(dsm + 16384));
+      constexpr uint32_t idesc = idesc_bf16(128, 128, 0, 0);
+      uint32_t ph = 0;
+      while (!done) {
+        for (int k = 0; k < 8; ++k) mma_ss_w(tmem_base + 256, da + 2 * k, db + 2 * k, idesc, k > 0);
+        mma_commit_w(&mbar);
+        mbar_wait(&mbar, ph);
+        ph ^= 1;
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tmem_base);
+    return;
+  }
   // warps w and w+4 share TMEM lane quarter (w & 3) (= SMSP); each owns 128 columns
   const uint32_t t = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * 128;
   {
@@ -55,7 +81,7 @@ __global__ void __launch_bounds__(256, 1) softmax_kernel(int iters, long long* c
     for (int c = 0; c < 4; ++c) tmem_st32(t + c * 32, init);
     tmem_wait_st();
   }
-  __syncthreads();
+  asm volatile("bar.sync 1, %0;" ::"r"(nsoft * 32));  // the softmax warps only (the MMA warp is looping)
   const float sl2 = 0.08838834764831845f * 1.4426950408889634f;
   float m_used = 0.f, l = 0.f;
   const long long t0 = clock64();
@@ -92,16 +118,19 @@ __global__ void __launch_bounds__(256, 1) softmax_kernel(int iters, long long* c
   const long long t1 = clock64();
   sink[blockIdx.x * blockDim.x + threadIdx.x] = l;
   if (lane == 0) cyc[blockIdx.x * 8 + warp] = t1 - t0;
+  asm volatile("bar.sync 1, %0;" ::"r"(nsoft * 32));
+  if (threadIdx.x == 0) done = 1;
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<256>(tmem_base);
+  if (warp == 0) tmem_dealloc<512>(tmem_base);
 }
 
 template <int EMU, int SUMS>
-void run(const char* name, int warps_per_smsp, long long* dcyc, float* sink) {
-  const int iters = 2000, threads = 128 * warps_per_smsp;
-  softmax_kernel<EMU, SUMS><<<148, threads>>>(iters, dcyc, sink);
-  softmax_kernel<EMU, SUMS><<<148, threads>>>(iters, dcyc, sink);
+void run(const char* name, int warps_per_smsp, long long* dcyc, float* sink, int mma = 0) {
+  const int iters = 2000, nsoft = 4 * warps_per_smsp, threads = 32 * (nsoft + 1);
+  cudaFuncSetAttribute(softmax_kernel<EMU, SUMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 + 1024);
+  softmax_kernel<EMU, SUMS><<<148, threads, 32768 + 1024>>>(iters, dcyc, sink, nsoft, mma);
+  softmax_kernel<EMU, SUMS><<<148, threads, 32768 + 1024>>>(iters, dcyc, sink, nsoft, mma);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148 * 8];
   cudaMemcpy(h, dcyc, sizeof h, cudaMemcpyDeviceToHost);
@@ -109,16 +138,17 @@ void run(const char* name, int warps_per_smsp, long long* dcyc, float* sink) {
   int n = 0;
   for (int b = 0; b < 148; ++b)
     for (int w = 0; w < 4 * warps_per_smsp; ++w) sum += h[b * 8 + w], ++n;
-  printf("{\"case\": \"%s\", \"warps_per_smsp\": %d, \"cycles_per_row_per_warp\": %.0f, \"err\": \"%s\"}\n", name,
-         warps_per_smsp, sum / n / iters, cudaGetErrorString(e));
+  printf("{\"case\": \"%s\", \"warps_per_smsp\": %d, \"mma_warp\": %d, \"cycles_per_row_per_warp\": %.0f, \"err\": \"%s\"}\n",
+         name, warps_per_smsp, mma, sum / n / iters, cudaGetErrorString(e));
 }
 
 int main() {
   long long* cyc;
   float* sink;
   cudaMalloc(&cyc, 148 * 8 * sizeof(long long));
-  cudaMalloc(&sink, 148 * 256 * sizeof(float));
+  cudaMalloc(&sink, 148 * 512 * sizeof(float));
   for (int w : {1, 2}) {
+    run<4, 1>("emu1of4 (kernel) + MMA stream", w, cyc, sink, 1);
     run<4, 1>("emu1of4 (kernel)", w, cyc, sink);
     run<0, 1>("all MUFU", w, cyc, sink);
     run<2, 1>("emu1of2", w, cyc, sink);
