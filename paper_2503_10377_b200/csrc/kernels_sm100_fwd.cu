@@ -44,6 +44,18 @@ constexpr int kEmuEvery = SPPO_EMU_EVERY;        // 1 of every kEmuEvery exp2 pa
 #define SPPO_WARP_ARRIVE 1  // P-ready signals as one arrival per warp after __syncwarp
 #endif
 constexpr bool kWarpArrive = SPPO_WARP_ARRIVE;
+#ifndef SPPO_FWD_TOKEN
+#define SPPO_FWD_TOKEN 0
+#endif
+// Option (off): the two tiles' softmax alternate — tile t runs its exponentials only
+// while holding its token (taken once its S is in TMEM, passed to the other tile once
+// its P is stored).  tools/softmax_bench.cu puts a lone softmax row at ~1200 cycles
+// per SMSP vs ~2000 when both tiles' softmax overlap, and the tiles drift into near
+// lockstep (period ~= 2000 + the ~900-cycle S(n+1) chain).  Measured: in the kernel a
+// lone row block still takes ~1740 cycles (first LD 140, first 64 exponentials 753,
+// row max 244, rest 601) + ~130 for the hand-over, so the period grows to ~3580-3830
+// (fwd 987 vs 1084-1090 TF/s): the overlap of the two tiles is worth more.
+constexpr bool kToken = SPPO_FWD_TOKEN;
 
 constexpr uint32_t kIdescS = idesc_bf16(128, 128, 0, 0);   // Q (K-major) x K (K-major)
 constexpr uint32_t kIdescPV = idesc_bf16(128, 128, 0, 1);  // P (TMEM) x V (MN-major)
@@ -55,6 +67,7 @@ struct Bars {
   uint64_t s_full[2];   // S_t ready in TMEM (per Q tile)
   uint64_t p_full[2][2];  // P_t keys [64h, 64h+64) written to TMEM (128 softmax threads arrive)
   uint64_t o_full[2];   // PV_t complete
+  uint64_t tok[2];      // softmax token of tile t (4 warps of the other tile arrive)
   uint32_t tmem_base;
 };
 
@@ -143,6 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       mbar_init(&bars.p_full[s][0], kWarpArrive ? 4 : 128);
       mbar_init(&bars.p_full[s][1], kWarpArrive ? 4 : 128);
       mbar_init(&bars.o_full[s], 1);
+      mbar_init(&bars.tok[s], 4);
     }
     fence_mbar_init();
   }
@@ -303,6 +317,13 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       // PV(n-1) completed before S(n) (same issuing thread, in-order pipe): consuming its
       // o_full phase here is free and keeps every mbarrier phase waited on (synccheck-clean)
       if (n > 0) mbar_wait(&bars.o_full[t], (n - 1) & 1);
+      // softmax token: tile 0 waits from its second row block on (phase n-1, passed by
+      // tile 1's softmax n-1), tile 1 from its first (phase n, passed by tile 0's n) —
+      // only while the other tile still has that row block (ragged diagonal CTAs).  A
+      // tile can pass at most one phase ahead of the other's wait (its next pass needs
+      // the other's), so the parity waits never alias.
+      if (kToken && (t == 1 ? n < T[0] : (n > 0 && n - 1 < T[1])))
+        mbar_wait(&bars.tok[t], (t == 1 ? n : n - 1) & 1);
       if (lane == 0 && wq == 0) TR(5 + 3 * t, n);
       tc_fence_after();
       uint32_t r[128];
@@ -314,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       tmem_ld32(sS + 32, R32(32));
       tmem_wait_ld_regs(R32(0));
       tmem_wait_ld_regs(R32(32));
+      if (lane == 0 && wq == 0 && t == 0) TR(13, n);  // (trace: first S half in registers)
       tmem_ld32(sS + 64, R32(64));
       tmem_ld32(sS + 96, R32(96));
       if (!split) {
@@ -362,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
         // speculative: the first 64 exponentials run against the stale max m_used
         // while the row max is computed alongside; only a (rare) rescale redoes them
         exps(0, -m_used, pk0, ls0);
+        if (lane == 0 && wq == 0 && t == 0) TR(14, n);  // (trace: first 64 exponentials done)
         if (split) {
           tmem_wait_ld_regs(R32(64));
           tmem_wait_ld_regs(R32(96));
@@ -409,6 +432,10 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
         if (lane == 0) mbar_arrive(&bars.p_full[t][1]);
       } else {
         mbar_arrive(&bars.p_full[t][1]);
+      }
+      if (kToken) {  // pass the token (P stored: this tile's MUFU work of row block n is done)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.tok[t ^ 1]);
       }
       l += ls0.x + ls0.y + ls1.x + ls1.y;
     }

@@ -31,8 +31,9 @@ if kind == "bwd":
     period_slot = 2
 else:
     names = ["vfull", "PV0", "S0+1", "PV1", "S1+1", "s0seen", "s0max", "p0full", "s1seen", "s1max", "p1full",
-             "ldK", "ldV", "-", "-", "-"]
-    pairs = [(5, 6), (6, 7), (8, 9), (9, 10), (1, 2), (3, 4), (7, 2), (10, 4), (2, 5), (4, 8)]
+             "ldK", "ldV", "s0ld", "s0exp64", "-"]
+    pairs = [(5, 6), (6, 7), (8, 9), (9, 10), (1, 2), (3, 4), (7, 2), (10, 4), (2, 5), (4, 8), (5, 13), (13, 14),
+             (14, 6)]
     period_slot = 2
 base = rows[0][1]
 for r in rows[:4] + rows[len(rows) // 2:len(rows) // 2 + 3]:
