@@ -15,7 +15,6 @@ namespace {
 
 constexpr int kWarps = 4;   // rows (fwd/dQ) or keys (dK/dV) per block, one warp each
 constexpr int kTile = 32;   // keys (or query rows) per smem tile: one per lane
-constexpr int kMaxD = 128;
 
 __device__ __forceinline__ float warp_max(float x) {
 #pragma unroll

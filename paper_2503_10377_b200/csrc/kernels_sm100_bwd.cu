@@ -91,6 +91,7 @@ static_assert(kSmemBytes <= 232448, "smem budget");
 #define SPPO_BWD_EMU_EVERY 0  // 1 of every N exp2 pairs of P on the FMA pipe (cubic, as the forward); 0 = off
 #endif
 constexpr int kBwdEmu = SPPO_BWD_EMU_EVERY;
+constexpr int kEmuDiv = kBwdEmu > 0 ? kBwdEmu : 1;  // (no modulo by zero when off)
 #ifndef SPPO_BWD_ROT
 #define SPPO_BWD_ROT 1  // measured: without the rotation bwd 985.6-986.0 vs 1042.0-1049.1 TF/s
 #endif
@@ -650,11 +651,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               x1.x = (jj + 2 >= first_vis) ? x1.x : -INFINITY;
               x1.y = (jj + 3 >= first_vis) ? x1.y : -INFINITY;
             }
-            if (kBwdEmu > 0 && c2 % kBwdEmu == kBwdEmu - 1)
+            if (kBwdEmu > 0 && c2 % kEmuDiv == kEmuDiv - 1)
               pr[c2] = ex2_poly2(x0);
             else
               pr[c2] = make_float2(ex2(x0.x), ex2(x0.y));
-            if (kBwdEmu > 0 && (c2 + 1) % kBwdEmu == kBwdEmu - 1)
+            if (kBwdEmu > 0 && (c2 + 1) % kEmuDiv == kEmuDiv - 1)
               pr[c2 + 1] = ex2_poly2(x1);
             else
               pr[c2 + 1] = make_float2(ex2(x1.x), ex2(x1.y));
