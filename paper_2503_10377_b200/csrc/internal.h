@@ -57,7 +57,12 @@ struct BwdParams {
   int32_t trace_life;         // debug: trace holds kLifeSlots stamps per CTA of the launch instead
 };
 
-// Debug tracing (env SPPO_TRACE=<file>): slot layout trace[iter * kTraceSlots + event]
+// Debug tracing (env SPPO_TRACE=<file>): slot layout trace[iter * kTraceSlots + event].
+// The clock64 stamps are compiled in only with -DSPPO_TRACE_BUILD=1 (tools/make_variant.sh):
+// even untaken, the stamp points constrain the instruction schedule of the hot loops.
+#ifndef SPPO_TRACE_BUILD
+#define SPPO_TRACE_BUILD 0  // measured: with the stamp points compiled in, fwd 1066 vs 1130-1136 TF/s
+#endif
 constexpr int kTraceSlots = 16;
 constexpr int kTraceIters = 512;
 // Lifetime mode (env SPPO_TRACE_LIFE=1, bwd only): trace[cta * kLifeSlots + k], cta =

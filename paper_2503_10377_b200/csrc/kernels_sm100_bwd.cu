@@ -256,7 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   unsigned long long* tr = (p.trace && !p.trace_life && blockIdx.x == 0) ? p.trace : nullptr;
 #define TR(slot, it)                                                              \
   do {                                                                            \
-    if (tr && (it) < kTraceIters) tr[(it) * kTraceSlots + (slot)] = clock64();   \
+    if (SPPO_TRACE_BUILD && tr && (it) < kTraceIters) tr[(it) * kTraceSlots + (slot)] = clock64();   \
   } while (0)
   if (threadIdx.x == 0) LIFE(1);
   int red_tiles = 0;  // Q tiles this CTA processed (lifetime trace)

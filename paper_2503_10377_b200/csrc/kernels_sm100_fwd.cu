@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
   unsigned long long* tr = (p.trace && blockIdx.x == 0 && blockIdx.y == 0) ? p.trace : nullptr;
 #define TR(slot, it)                                                            \
   do {                                                                          \
-    if (tr && (it) < kTraceIters) tr[(it) * kTraceSlots + (slot)] = clock64(); \
+    if (SPPO_TRACE_BUILD && tr && (it) < kTraceIters) tr[(it) * kTraceSlots + (slot)] = clock64(); \
   } while (0)
 
   // register budget per warpgroup: control WG 56, softmax WGs 224 (no merge of the

@@ -1,6 +1,8 @@
 """Run one C2-shaped step with SPPO_TRACE set (kernel event timestamps of CTA
 (0,0) of one launch, see csrc/*.cu TR(...) points) and print a per-iteration
-timeline summary.  Env: SPPO_TRACE=<file> SPPO_TRACE_CHUNK=<i> SPPO_TRACE_KIND=fwd|bwd."""
+timeline summary.  Env: SPPO_TRACE=<file> SPPO_TRACE_CHUNK=<i> SPPO_TRACE_KIND=fwd|bwd.
+Needs a build with the stamp points compiled in (they cost the forward ~6 % even
+untaken): tools/make_variant.sh tr -DSPPO_TRACE_BUILD=1, then run from tmp_tr/."""
 import os
 import statistics
 import sys
