@@ -44,6 +44,10 @@ constexpr int kEmuEvery = SPPO_EMU_EVERY;        // 1 of every kEmuEvery exp2 pa
 #define SPPO_WARP_ARRIVE 1  // P-ready signals as one arrival per warp after __syncwarp
 #endif
 constexpr bool kWarpArrive = SPPO_WARP_ARRIVE;
+#ifndef SPPO_FWD_SPEC
+#define SPPO_FWD_SPEC 0  // 1: first 64 exponentials against the stale row max, redone on a rescale (fwd -1 %)
+#endif
+constexpr bool kSpec = SPPO_FWD_SPEC;
 #ifndef SPPO_FWD_TOKEN
 #define SPPO_FWD_TOKEN 0
 #endif
@@ -379,6 +383,34 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_kernel(const __grid_constant_
       if (n == 0 && p.first) {
         const float mx = row_max();
         m_used = (mx == -INFINITY) ? 0.f : mx;
+        exps(0, -m_used, pk0, ls0);
+      } else if (!kSpec) {
+        // max first (all 128 columns loaded), then the exponentials once.  Measured
+        // against the speculative order below (interleaved, trace points out): fwd
+        // 1127-1154 vs 1109-1137 TF/s — one exponential path schedules better.
+        if (split) {
+          tmem_wait_ld_regs(R32(64));
+          tmem_wait_ld_regs(R32(96));
+        }
+        const float mx = row_max();
+        const bool need = mx > m_used + kRescaleThreshold;
+        if (__any_sync(0xffffffffu, need)) {
+          const float f = need ? ex2(m_used - mx) : 1.f;
+          if (need) {
+            m_used = mx;
+            l *= f;
+          }
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) {
+            uint32_t o[32];
+            tmem_ld32(sO + cb * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * f);
+            tmem_st32(sO + cb * 32, o);
+          }
+          tmem_wait_st();
+        }
         exps(0, -m_used, pk0, ls0);
       } else {
         // speculative: the first 64 exponentials run against the stale max m_used
