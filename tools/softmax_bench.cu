@@ -38,6 +38,14 @@ __device__ __forceinline__ void exps64(const float* s, int j0, float negm, float
   if (SUMS == 2) lsum = fadd2(lsum, l2);
 }
 
+// -DSTAMPS=1: clock64 stamps per phase of warp 0 of CTA 0 (ld, exps 1, max, exps 2 +
+// stores).  The stamps themselves change the schedule: 1762 vs 1197 cycles per row —
+// which is how the kernels' (untaken) trace points were found to cost the forward 6 %.
+#ifndef STAMPS
+#define STAMPS 0
+#endif
+__device__ long long g_phase[4];
+
 template <int EMU, int SUMS>
 __global__ void __launch_bounds__(288, 1) softmax_kernel(int iters, long long* cyc, float* sink, int nsoft, int mma) {
   __shared__ uint32_t tmem_base;
@@ -85,7 +93,10 @@ __global__ void __launch_bounds__(288, 1) softmax_kernel(int iters, long long* c
   const float sl2 = 0.08838834764831845f * 1.4426950408889634f;
   float m_used = 0.f, l = 0.f;
   const long long t0 = clock64();
+  long long ph[4] = {0, 0, 0, 0};
+  const bool stamp = STAMPS && blockIdx.x == 0 && warp == 0;
   for (int it = 0; it < iters; ++it) {
+    long long c0 = stamp ? clock64() : 0;
     uint32_t r[128];
     auto R32 = [&](int c) -> uint32_t(&)[32] { return *reinterpret_cast<uint32_t(*)[32]>(&r[c]); };
     tmem_ld32(t + 0, R32(0));
@@ -97,7 +108,9 @@ __global__ void __launch_bounds__(288, 1) softmax_kernel(int iters, long long* c
     float* s = reinterpret_cast<float*>(r);
     uint32_t pk0[32];
     float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
+    long long c1 = stamp ? clock64() : 0;
     exps64<EMU, SUMS>(s, 0, -m_used, sl2, pk0, ls0);
+    long long c2 = stamp ? clock64() : 0;
     tmem_wait_ld_regs(R32(64));
     tmem_wait_ld_regs(R32(96));
     float mx0 = s[0], mx1 = s[1];
@@ -108,14 +121,24 @@ __global__ void __launch_bounds__(288, 1) softmax_kernel(int iters, long long* c
     }
     const float mx = fmax3(mx0, mx1, fmaxf(s[126], s[127])) * sl2;
     if (__any_sync(0xffffffffu, mx > m_used + 8.f)) m_used = mx;  // (never: data in [-0.5, 0.5])
+    long long c3 = stamp ? clock64() : 0;
     tmem_st32(t + 0, pk0);
     tmem_wait_st();
     exps64<EMU, SUMS>(s, 64, -m_used, sl2, &r[32], ls1);
     tmem_st32(t + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
     tmem_wait_st();
     l += ls0.x + ls0.y + ls1.x + ls1.y;
+    if (stamp) {
+      const long long c4 = clock64();
+      ph[0] += c1 - c0;
+      ph[1] += c2 - c1;
+      ph[2] += c3 - c2;
+      ph[3] += c4 - c3;
+    }
   }
   const long long t1 = clock64();
+  if (stamp && lane == 0)
+    for (int k = 0; k < 4; ++k) g_phase[k] = ph[k] / iters;
   sink[blockIdx.x * blockDim.x + threadIdx.x] = l;
   if (lane == 0) cyc[blockIdx.x * 8 + warp] = t1 - t0;
   asm volatile("bar.sync 1, %0;" ::"r"(nsoft * 32));
@@ -138,8 +161,11 @@ void run(const char* name, int warps_per_smsp, long long* dcyc, float* sink, int
   int n = 0;
   for (int b = 0; b < 148; ++b)
     for (int w = 0; w < 4 * warps_per_smsp; ++w) sum += h[b * 8 + w], ++n;
-  printf("{\"case\": \"%s\", \"warps_per_smsp\": %d, \"mma_warp\": %d, \"cycles_per_row_per_warp\": %.0f, \"err\": \"%s\"}\n",
-         name, warps_per_smsp, mma, sum / n / iters, cudaGetErrorString(e));
+  long long ph[4];
+  cudaMemcpyFromSymbol(ph, g_phase, sizeof ph);
+  printf("{\"case\": \"%s\", \"warps_per_smsp\": %d, \"mma_warp\": %d, \"cycles_per_row_per_warp\": %.0f, "
+         "\"phases_warp0\": {\"ld\": %lld, \"exps1\": %lld, \"max\": %lld, \"exps2_st\": %lld}, \"err\": \"%s\"}\n",
+         name, warps_per_smsp, mma, sum / n / iters, ph[0], ph[1], ph[2], ph[3], cudaGetErrorString(e));
 }
 
 int main() {
