@@ -92,6 +92,20 @@ static_assert(kSmemBytes <= 232448, "smem budget");
 #endif
 constexpr int kBwdEmu = SPPO_BWD_EMU_EVERY;
 constexpr int kEmuDiv = kBwdEmu > 0 ? kBwdEmu : 1;  // (no modulo by zero when off)
+// register budget per role (the launch gives 128 per thread: 512 x 128 = 65536).
+// Measured: compute 160 / control 56 -> bwd 1022-1027, compute 152 / control 72 ->
+// 1075-1080 vs 1103 TF/s (the MMA / producer warps spill).
+#ifndef SPPO_BWD_REGS_COMP
+#define SPPO_BWD_REGS_COMP 136  // compute warps 4-11
+#endif
+#ifndef SPPO_BWD_REGS_RED
+#define SPPO_BWD_REGS_RED 136   // dQ reducer warps 0-3
+#endif
+#ifndef SPPO_BWD_REGS_CTRL
+#define SPPO_BWD_REGS_CTRL 104  // MMA issuer + TMA producers, warps 12-15
+#endif
+static_assert(256 * SPPO_BWD_REGS_COMP + 128 * SPPO_BWD_REGS_RED + 128 * SPPO_BWD_REGS_CTRL <= 512 * 128,
+              "setmaxnreg budget exceeds the launch's register allocation (the increase would never complete)");
 #ifndef SPPO_BWD_ROT
 #define SPPO_BWD_ROT 1  // measured: without the rotation bwd 985.6-986.0 vs 1042.0-1049.1 TF/s
 #endif
@@ -268,7 +282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   };
 
   if (warp >= 12) {
-    setmaxnreg_dec<104>();
+    setmaxnreg_dec<SPPO_BWD_REGS_CTRL>();
     if (warp == 13) {
       // ===================== TMA: K, V once per item; Q rows half + LSE per tile =====================
       const CUtensorMap* mq64 = tmap(a, a.q64_slot);
@@ -500,7 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp < 4) {
-    setmaxnreg_inc<136>();
+    setmaxnreg_inc<SPPO_BWD_REGS_RED>();
     // ===================== dQ reducer + item epilogue (TMEM lane = q row / key row) =====================
     const CUtensorMap* mdq = tmap(a, a.dq_slot);
     const float tau = p.scale;
@@ -599,7 +613,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) bulk_wait<0>();
     red_tiles = gt;
   } else {
-    setmaxnreg_inc<136>();
+    setmaxnreg_inc<SPPO_BWD_REGS_COMP>();
     // ===================== compute: P and dS (TMEM lane = key row) =====================
     const int g = (warp - 4) >> 2;  // column half: q in [64g, 64g+64)
     const int wq = warp & 3;
